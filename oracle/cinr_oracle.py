@@ -1,0 +1,765 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+CPU restatement of the reference cached-INR ray-march path
+(`voxcache`, /root/reference/pkg/src/voxcache) in numpy + the plain-C loops of
+oracle_kernels.c.  Only tests/, __graft_entry__.smoke() and bench.py's CPU arms
+may import this module; the product package never does.
+
+Pinned against the real reference by tests/test_oracle_golden.py, which replays
+the fixtures tests/golden/make_golden.py recorded from `voxcache` itself
+(per-frame page tables, pool owners/stamps, request tables, dispatched batches,
+FrameRecord counters and images).
+
+Every function cites the reference file:line it restates (paths relative to
+pkg/src/voxcache/).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import time
+from dataclasses import dataclass, field as dc_field
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB = None
+
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+u8p = C.POINTER(C.c_uint8)
+i8p = C.POINTER(C.c_int8)
+i32p = C.POINTER(C.c_int32)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        so = _HERE / "_build" / "liboracle.so"
+        src = _HERE / "oracle_kernels.c"
+        if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+            subprocess.check_call([str(_HERE / "build_oracle.sh")])
+        _LIB = C.CDLL(str(so))
+    return _LIB
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+class _AdvArgs(C.Structure):
+    _fields_ = [("o", f64p), ("d", f64p), ("t_en", f64p), ("t_ex", f64p), ("cursor_f", f64p),
+                ("cursor_k", i64p), ("active", u8p), ("adaptive", C.c_int), ("skip_empty", C.c_int),
+                ("dt_base", C.c_double), ("mu_floor", C.c_double), ("mu", f32p),
+                ("gx", C.c_int64), ("gy", C.c_int64), ("gz", C.c_int64),
+                ("cwx", C.c_double), ("cwy", C.c_double), ("cwz", C.c_double),
+                ("out_pos", f64p), ("out_dt", f64p), ("out_tmid", f64p), ("sample_mask", u8p), ("done_mask", u8p)]
+
+
+class _ProbeArgs(C.Structure):
+    _fields_ = [("pos", f64p), ("dist", f64p), ("u", f64p), ("lod_scale", C.c_double), ("mode", C.c_int),
+                ("vx", C.c_double), ("vy", C.c_double), ("vz", C.c_double), ("max_lod", C.c_int64), ("b", C.c_int64),
+                ("table", i32p), ("offsets", i64p), ("grids", i64p), ("pool", f32p), ("last_used", i64p),
+                ("frame", C.c_int64), ("values", f32p), ("served", i8p), ("req", i8p)]
+
+
+class _InrArgs(C.Structure):
+    _fields_ = [("levels", C.c_int64), ("feats", C.c_int64), ("res", i64p), ("dense", u8p), ("tab_off", i64p),
+                ("table_size", C.c_int64), ("tables", f32p), ("n_layers", C.c_int64), ("dims", i64p),
+                ("W", C.POINTER(f32p)), ("B", C.POINTER(f32p)), ("out_sigmoid", C.c_int)]
+
+
+# ----------------------------------------------------------------- operator passes
+def raygen_pass(base, rot, origin, tan_h, tan_v, dirs, t0, t1, keep):
+    """kernels.py:426 raygen_pass (arrays caller-allocated, written in place)."""
+    keep_u8 = keep.view(np.uint8)
+    lib().orc_raygen(C.c_int64(base.shape[0]), _p(base, f64p), _p(np.ascontiguousarray(rot), f64p),
+                     _p(np.ascontiguousarray(origin, dtype=np.float64), f64p), C.c_double(tan_h), C.c_double(tan_v),
+                     _p(dirs, f64p), _p(t0, f64p), _p(t1, f64p), _p(keep_u8, u8p))
+
+
+def advance_pass(o, d, t_en, t_ex, cursor_f, cursor_k, active, adaptive, skip_empty, dt_base, mu_floor,
+                 mu_flat, gx, gy, gz, cwx, cwy, cwz, out_pos, out_dt, out_tmid, sample_mask, done_mask):
+    """kernels.py:160 advance_pass."""
+    a = _AdvArgs(_p(o, f64p), _p(d, f64p), _p(t_en, f64p), _p(t_ex, f64p), _p(cursor_f, f64p), _p(cursor_k, i64p),
+                 _p(active.view(np.uint8), u8p), int(adaptive), int(skip_empty), dt_base, mu_floor,
+                 _p(mu_flat, f32p), gx, gy, gz, cwx, cwy, cwz, _p(out_pos, f64p), _p(out_dt, f64p),
+                 _p(out_tmid, f64p), _p(sample_mask.view(np.uint8), u8p), _p(done_mask.view(np.uint8), u8p))
+    lib().orc_advance(C.c_int64(o.shape[0]), C.byref(a))
+
+
+def probe_pass(pos, dist, u, lod_scale, mode, vx, vy, vz, max_lod, b, table_flat, offsets, grids, pool_flat,
+               last_used, frame, values, served, req):
+    """kernels.py:316 probe_pass -> (exact, fallback, miss)."""
+    a = _ProbeArgs(_p(pos, f64p), _p(dist, f64p), _p(u, f64p), lod_scale, mode, vx, vy, vz, max_lod, b,
+                   _p(table_flat, i32p), _p(offsets, i64p), _p(np.ascontiguousarray(grids, dtype=np.int64), i64p),
+                   _p(pool_flat, f32p), _p(last_used, i64p), frame, _p(values, f32p), _p(served, i8p), _p(req, i8p))
+    counts = np.zeros(3, dtype=np.int64)
+    lib().orc_probe(C.c_int64(pos.shape[0]), C.byref(a), _p(counts, i64p))
+    return int(counts[0]), int(counts[1]), int(counts[2])
+
+
+def shade_pass(rows, values, dt, lut, adaptive, dt_base, term, color, trans, dead):
+    """kernels.py:370 shade_pass."""
+    lib().orc_shade(C.c_int64(rows.shape[0]), _p(rows, i64p), _p(values, f32p), _p(dt, f64p), _p(lut, f32p),
+                    C.c_int64(lut.shape[0]), int(adaptive), C.c_double(dt_base), C.c_double(term),
+                    _p(color, f64p), _p(trans, f64p), _p(dead.view(np.uint8), u8p))
+
+
+# ----------------------------------------------------------------- brick math
+def grid_axis(v, b, lod):
+    """brickmath.py:48-53."""
+    s = 1 << lod
+    if v <= (b - 1) * s + 1:
+        return 1
+    return -(-(v + s) // (b << lod))
+
+
+def layout_grids(dims, b):
+    """brickmath.py:60-67 max_lod + per-LoD grids (BrickLayout 87-99)."""
+    if b < 2:
+        raise ValueError("brick_size must be >= 2")
+    grids = []
+    lod = 0
+    while True:
+        g = tuple(grid_axis(int(v), b, lod) for v in dims)
+        grids.append(g)
+        if g == (1, 1, 1):
+            return lod, grids
+        lod += 1
+        if lod > 48:
+            raise ValueError("no single-brick LoD")
+
+
+def brick_origin(idx, b, lod):
+    """brickmath.py:35-39: k*B*2^L - 1 for k>0, else 0."""
+    idx = np.asarray(idx, dtype=np.int64)
+    o = idx * (b << lod)
+    return np.where(idx > 0, o - 1, o)
+
+
+def brick_positions(dims, b, lod, index):
+    """brickmath.py:125-139 sample_positions: x-fastest, clipped, (n+0.5)/V."""
+    ax = np.arange(b, dtype=np.int64) << lod
+    org = brick_origin(index, b, lod)
+    zz, yy, xx = np.meshgrid(ax, ax, ax, indexing="ij")
+    nat = np.stack([xx.ravel(), yy.ravel(), zz.ravel()], axis=1) + org
+    np.clip(nat, 0, np.asarray(dims, dtype=np.int64) - 1, out=nat)
+    return nat, (nat + 0.5) / np.asarray(dims, dtype=np.float64)
+
+
+def locate(pos, b, lod, grid):
+    """brickmath.py:42-45 + 105-120: floor((p+1)/span) clamped; local clamped to [0,B-1]."""
+    span = b << lod
+    idx = np.floor((np.asarray(pos, dtype=np.float64) + 1.0) / span).astype(np.int64)
+    np.clip(idx, 0, np.asarray(grid, dtype=np.int64) - 1, out=idx)
+    local = (pos - brick_origin(idx, b, lod)) / (1 << lod)
+    np.clip(local, 0.0, b - 1, out=local)
+    return idx, local
+
+
+# ----------------------------------------------------------------- rng / lod
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+
+
+def splitmix64(x):
+    """sampler.py:24-30 (uint64 wrap)."""
+    with np.errstate(over="ignore"):
+        z = (np.asarray(x, dtype=np.uint64) + GOLDEN).astype(np.uint64)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def lane_seeds(seed, frame, lanes):
+    """sampler.py:39-45 XorShift32.seed_frame."""
+    with np.errstate(over="ignore"):
+        base = splitmix64(np.uint64(seed & 0xFFFFFFFFFFFFFFFF) ^ (np.uint64(frame) * GOLDEN))
+        s = (splitmix64(base + np.arange(lanes, dtype=np.uint64)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    s[s == 0] = np.uint32(0x9E3779B9)
+    return s
+
+
+def xorshift_uniform(state, n):
+    """sampler.py:51-58: advance the first n lanes, u = x / 2^32."""
+    x = state[:n]
+    x = x ^ (x << np.uint32(13))
+    x = x ^ (x >> np.uint32(17))
+    x = x ^ (x << np.uint32(5))
+    state[:n] = x
+    return x.astype(np.float64) / 4294967296.0
+
+
+def effective_scale(lod_scale, preload, frame, force):
+    """sampler.py:70-77."""
+    if frame >= preload or force <= lod_scale:
+        return lod_scale
+    return lod_scale + (force - lod_scale) * (1.0 - frame / preload)
+
+
+def dist_to_unit_box(p):
+    """sampler.py:283-285."""
+    gap = np.maximum(np.maximum(-p, p - 1.0), 0.0)
+    return float(np.linalg.norm(gap))
+
+
+# ----------------------------------------------------------------- fields
+class LatticeField:
+    """fields.py:202-221 RawLatticeField (trilinear, C loop)."""
+
+    def __init__(self, lattice):
+        self.lattice = np.ascontiguousarray(lattice, dtype=np.float32)
+        vz, vy, vx = self.lattice.shape
+        self.dims = (vx, vy, vz)
+
+    def sample(self, pos):
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        out = np.empty(pos.shape[0], dtype=np.float32)
+        vx, vy, vz = self.dims
+        lib().orc_lattice_sample(C.c_int64(pos.shape[0]), _p(pos, f64p), _p(self.lattice, f32p), C.c_int64(vx),
+                                 C.c_int64(vy), C.c_int64(vz), _p(out, f32p))
+        return out
+
+    def lattice_values(self):
+        return self.lattice
+
+
+class InrFieldOracle:
+    """inr/model.py:65-89 InrModel.infer_batch + InrField clip; encoding.py:91-134, mlp.py:39-53."""
+
+    def __init__(self, dims, tables, weights, biases, grid_cfg, out_sigmoid=True):
+        self.dims = tuple(dims)
+        self.levels = grid_cfg["levels"]
+        self.feats = grid_cfg["features_per_entry"]
+        self.table_size = grid_cfg["table_size"]
+        res = [int(np.floor(grid_cfg["base_resolution"] * grid_cfg["growth_factor"] ** l)) for l in range(self.levels)]
+        self.res = np.array(res, dtype=np.int64)
+        self.dense = np.array([(r + 1) ** 3 <= self.table_size for r in res], dtype=np.uint8)
+        rows = [t.shape[0] for t in tables]
+        self.tab_off = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(np.int64)
+        self.tables = np.ascontiguousarray(np.concatenate(tables, axis=0), dtype=np.float32)
+        self.W = [np.ascontiguousarray(w, dtype=np.float32) for w in weights]
+        self.B = [np.ascontiguousarray(b, dtype=np.float32) for b in biases]
+        self.ldims = np.array([self.W[0].shape[1]] + [w.shape[0] for w in self.W], dtype=np.int64)
+        self._wp = (f32p * len(self.W))(*[_p(w, f32p) for w in self.W])
+        self._bp = (f32p * len(self.B))(*[_p(b, f32p) for b in self.B])
+        self.args = _InrArgs(self.levels, self.feats, _p(self.res, i64p), _p(self.dense, u8p), _p(self.tab_off, i64p),
+                             self.table_size, _p(self.tables, f32p), len(self.W), _p(self.ldims, i64p),
+                             self._wp, self._bp, int(out_sigmoid))
+
+    def encode(self, pos):
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        feat = np.empty((pos.shape[0], self.levels * self.feats), dtype=np.float32)
+        lib().orc_inr_encode(C.c_int64(pos.shape[0]), _p(pos, f64p), C.byref(self.args), _p(feat, f32p))
+        return feat
+
+    def infer(self, pos):
+        feat = self.encode(pos)
+        out = np.empty(feat.shape[0], dtype=np.float32)
+        lib().orc_inr_mlp(C.c_int64(feat.shape[0]), _p(feat, f32p), C.byref(self.args), _p(out, f32p))
+        if not np.isfinite(out).all():
+            raise FloatingPointError("non-finite INR output")
+        return out
+
+    def sample(self, pos):
+        pos = np.asarray(pos, dtype=np.float64)
+        if pos.size and ((pos < 0.0).any() or (pos >= 1.0).any()):
+            raise ValueError("coordinate outside [0,1)^3")
+        if pos.shape[0] == 0:
+            return np.zeros(0, dtype=np.float32)
+        return np.clip(self.infer(pos), 0.0, 1.0).astype(np.float32)
+
+    def lattice_values(self):
+        """fields.py:100-116 sample_lattice at voxel centres, (Vz,Vy,Vx)."""
+        vx, vy, vz = self.dims
+        zs, ys, xs = np.meshgrid((np.arange(vz) + 0.5) / vz, (np.arange(vy) + 0.5) / vy,
+                                 (np.arange(vx) + 0.5) / vx, indexing="ij")
+        pos = np.stack([xs.ravel(), ys.ravel(), zs.ravel()], axis=1)
+        return self.sample(pos).reshape(vz, vy, vx)
+
+
+def inr_params_from_seed(grid_cfg, mlp_cfg, seed=0, redraw=42):
+    """inr/model.py:17-36 + mlp.py:28-36 parameter draw order; the config-1 redraw
+    uniform(-0.7,0.7) from default_rng(42) over (tables, weights, biases)."""
+    rng = np.random.default_rng(seed)
+    nf = grid_cfg["features_per_entry"]
+    tables = []
+    for l in range(grid_cfg["levels"]):
+        r = int(np.floor(grid_cfg["base_resolution"] * grid_cfg["growth_factor"] ** l))
+        ent = (r + 1) ** 3 if (r + 1) ** 3 <= grid_cfg["table_size"] else grid_cfg["table_size"]
+        tables.append(rng.uniform(-1e-4, 1e-4, size=(ent, nf)).astype(np.float32))
+    dims = [grid_cfg["levels"] * nf] + [mlp_cfg["hidden_width"]] * mlp_cfg["hidden_layers"] + [1]
+    weights, biases = [], []
+    for fi, fo in zip(dims[:-1], dims[1:]):
+        bound = 1.0 / np.sqrt(fi)
+        weights.append(rng.uniform(-bound, bound, size=(fo, fi)).astype(np.float32))
+        biases.append(np.zeros(fo, dtype=np.float32))
+    params = tables + weights + biases
+    if redraw is not None:
+        r = np.random.default_rng(redraw)
+        params = [r.uniform(-0.7, 0.7, size=p.shape).astype(np.float32) for p in params]
+    nt, nw = len(tables), len(weights)
+    return params[:nt], params[nt:nt + nw], params[nt + nw:]
+
+
+DEFAULT_GRID = dict(levels=8, features_per_entry=2, base_resolution=4, growth_factor=1.5, table_size=1 << 16)
+DEFAULT_MLP = dict(hidden_width=32, hidden_layers=2)
+
+
+# ----------------------------------------------------------------- transfer / macro
+def tf_eval(points, values):
+    """render/transfer.py:28-35."""
+    v = np.clip(np.asarray(values, dtype=np.float64), 0.0, 1.0)
+    return np.stack([np.interp(v, points[:, 0], points[:, c + 1]) for c in range(4)], axis=-1)
+
+
+def tf_lut(points, size=1024):
+    """render/transfer.py:37-43."""
+    return tf_eval(points, np.linspace(0.0, 1.0, size)).astype(np.float32)
+
+
+def warm_body_points(threshold=0.35, max_opacity=0.9):
+    """render/transfer.py:88-98."""
+    t = float(np.clip(threshold, 0.01, 0.95))
+    return np.array([[0.0, 0.0, 0.0, 0.1, 0.0], [t, 0.1, 0.05, 0.3, 0.0],
+                     [min(t + 0.15, 0.97), 0.9, 0.45, 0.1, 0.55 * max_opacity],
+                     [1.0, 1.0, 0.95, 0.8, max_opacity]], dtype=np.float64)
+
+
+def grayscale_points(max_opacity=1.0):
+    """render/transfer.py:80-81."""
+    return np.array([[0.0, 0, 0, 0, 0.0], [1.0, 1, 1, 1, max_opacity]], dtype=np.float64)
+
+
+def macro_minmax(lattice, cell):
+    """macrocell.py:49-74: per-cell min/max over the cell dilated by one voxel."""
+    vz, vy, vx = lattice.shape
+    g = [-(-v // cell) for v in (vx, vy, vz)]
+    vmin = np.empty((g[2], g[1], g[0]), dtype=np.float32)
+    vmax = np.empty_like(vmin)
+    for k in range(g[2]):
+        z0, z1 = max(k * cell - 1, 0), min((k + 1) * cell + 1, vz)
+        for j in range(g[1]):
+            y0, y1 = max(j * cell - 1, 0), min((j + 1) * cell + 1, vy)
+            for i in range(g[0]):
+                x0, x1 = max(i * cell - 1, 0), min((i + 1) * cell + 1, vx)
+                blk = lattice[z0:z1, y0:y1, x0:x1]
+                vmin[k, j, i] = blk.min()
+                vmax[k, j, i] = blk.max()
+    return vmin, vmax
+
+
+def majorants(points, vmin, vmax, bins=256):
+    """macrocell.py:105-128: TF opacity upper bound per value bin, range-max per cell.
+    (A direct max over the inclusive bin range equals the sparse-table query.)"""
+    edges = np.linspace(0.0, 1.0, bins + 1)
+    xs = np.unique(np.concatenate([edges, points[:, 0]]))
+    alphas = tf_eval(points, xs)[:, 3]
+    bin_of = np.minimum((xs * bins).astype(np.int64), bins - 1)
+    bmax = np.zeros(bins, dtype=np.float64)
+    np.maximum.at(bmax, bin_of, alphas)
+    on_edge = np.isclose(xs * bins, np.round(xs * bins)) & (xs > 0)
+    left = np.clip(np.round(xs * bins).astype(np.int64) - 1, 0, bins - 1)
+    np.maximum.at(bmax, left[on_edge], alphas[on_edge])
+    lo = np.clip((vmin.ravel() * bins).astype(np.int64), 0, bins - 1)
+    hi = np.clip((vmax.ravel() * bins).astype(np.int64), 0, bins - 1)
+    # prefix-free range max: build a dense [bins, bins] table once (bins=256)
+    rm = np.empty((bins, bins), dtype=np.float64)
+    for a in range(bins):
+        rm[a, a:] = np.maximum.accumulate(bmax[a:])
+    mu = rm[lo, np.maximum(hi, lo)]
+    return mu.reshape(vmin.shape).astype(np.float32)
+
+
+# ----------------------------------------------------------------- camera
+def camera_setup(position, target, up, fov_y, width, height):
+    """render/camera.py:36-42 basis + 129-138 generate_rays setup."""
+    fwd = np.asarray(target, dtype=np.float64) - np.asarray(position, dtype=np.float64)
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(up, dtype=np.float64))
+    right /= np.linalg.norm(right)
+    upv = np.cross(right, fwd)
+    rot = np.ascontiguousarray(np.stack([right, upv, fwd], axis=1))
+    tan_half = np.tan(np.radians(fov_y) / 2.0)
+    aspect = width / height
+    return rot, tan_half * aspect, tan_half
+
+
+def film_coords(width, height):
+    """render/camera.py:116-126."""
+    px = (np.arange(width) + 0.5) / width * 2.0 - 1.0
+    py = 1.0 - (np.arange(height) + 0.5) / height * 2.0
+    xs, ys = np.meshgrid(px, py)
+    return np.ascontiguousarray(np.stack([xs.ravel(), ys.ravel()], axis=1))
+
+
+def orbit_camera(center, radius, frames, frame, elevation_deg=20.0, phase=0.0):
+    """harness.py:45-57."""
+    import math
+
+    az = 2.0 * math.pi * frame / frames + phase
+    el = math.radians(elevation_deg)
+    off = np.array([math.cos(el) * math.cos(az), math.sin(el), math.cos(el) * math.sin(az)]) * radius
+    return tuple(np.asarray(center, dtype=np.float64) + off)
+
+
+# ----------------------------------------------------------------- cache + scheduler
+@dataclass
+class Config:
+    dims: tuple
+    brick: int = 40
+    pool: tuple = (8, 8, 8)
+    direct_threshold: int = 1 << 18
+    max_requests: int = 40
+    ranking: bool = True
+    rank_clamp: int = 1000
+    lod_scale: float = 1.0
+    preload: int = 120
+    mode: str = "corrected"
+    cached: bool = True
+    seed: int = 0
+    base_step_scale: float = 0.5
+    mu_floor: float = 1.0 / 16.0
+    term: float = 0.01
+    background: tuple = (0.0, 0.0, 0.0)
+    skip_empty: bool = True
+    adaptive: bool = True
+    max_iterations: int = 8192
+    macro_cell: int = 16
+
+
+class OracleCache:
+    """cache/mrpd.py:54-279 + pool.py:36-78 + pagetable.py (dense logical view, P13)."""
+
+    def __init__(self, cfg: Config):
+        self.cfg = cfg
+        self.b = cfg.brick
+        self.max_lod, self.grids = layout_grids(cfg.dims, cfg.brick)
+        counts = [g[0] * g[1] * g[2] for g in self.grids]
+        self.offsets = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+        self.total = int(sum(counts))
+        self.paged = any(c > cfg.direct_threshold for c in counts)
+        self.grids_arr = np.array(self.grids, dtype=np.int64)
+        self.slots = int(np.prod(cfg.pool))
+        self.frame = 0
+        self.reset()
+
+    def reset(self):
+        """mrpd.py:268-276 (keeps self.frame)."""
+        b = self.b
+        self.table = np.full(self.total, -1, dtype=np.int32)
+        self.pool = np.zeros(self.slots * b ** 3, dtype=np.float32)
+        self.owner = np.full((self.slots, 2), -1, dtype=np.int64)
+        self.last_used = np.full(self.slots, -1, dtype=np.int64)
+        self.free = list(range(self.slots - 1, -1, -1))
+        self.miss = {}
+        self.loaded_total = 0
+        self.stats = dict(requests=0, exact=0, fallback=0, miss=0, deferred=0, inserted=0)
+
+    def linear(self, lod, idx):
+        g = self.grids[lod]
+        return int(idx[0] + g[0] * (idx[1] + g[1] * idx[2]))
+
+    def unlinear(self, lod, lin):
+        g = self.grids[lod]
+        return (lin % g[0], (lin // g[0]) % g[1], lin // (g[0] * g[1]))
+
+    def is_mapped(self, lod, lin):
+        return self.table[self.offsets[lod] + lin] >= 0
+
+    def record_misses(self, native, req):
+        """mrpd.py:215-225 _record_misses (np.unique aggregation)."""
+        for lod in np.unique(req):
+            sel = req == lod
+            idx, _ = locate(native[sel], self.b, int(lod), self.grids[int(lod)])
+            uq, cnt = np.unique(idx, axis=0, return_counts=True)
+            for (i, j, k), c in zip(uq, cnt):
+                key = (int(lod), self.linear(int(lod), (i, j, k)))
+                self.miss[key] = self.miss.get(key, 0) + int(c)
+
+    def acquire(self, frame):
+        """pool.py:55-62."""
+        if self.free:
+            return self.free.pop()
+        cand = np.flatnonzero(self.last_used < frame)
+        if cand.size == 0:
+            return None
+        return int(cand[np.argmin(self.last_used[cand])])
+
+    def insert(self, key, samples, frame):
+        """mrpd.py:229-256."""
+        lod, lin = key
+        cur = int(self.table[self.offsets[lod] + lin])
+        b3 = self.b ** 3
+        if cur >= 0:
+            self.pool[cur * b3:(cur + 1) * b3] = samples
+            self.owner[cur] = key
+            self.last_used[cur] = frame
+            return cur
+        slot = self.acquire(frame)
+        if slot is None:
+            self.stats["deferred"] += 1
+            return None
+        if self.owner[slot, 0] >= 0:
+            ol, olin = self.owner[slot]
+            self.table[self.offsets[ol] + olin] = -1
+        self.pool[slot * b3:(slot + 1) * b3] = samples
+        self.owner[slot] = key
+        self.last_used[slot] = frame
+        self.table[self.offsets[lod] + lin] = slot
+        self.stats["inserted"] += 1
+        self.loaded_total += 1
+        return slot
+
+    def tick(self):
+        """mrpd.py:258-261."""
+        self.frame += 1
+        self.stats = dict(requests=0, exact=0, fallback=0, miss=0, deferred=0, inserted=0)
+
+    def occupancy(self):
+        return 1.0 - len(self.free) / self.slots
+
+
+class OracleRequests:
+    """scheduler.py:43-101 RequestTable (entries keyed by (lod, linear))."""
+
+    def __init__(self, cache: OracleCache, cfg: Config):
+        self.cache = cache
+        self.cfg = cfg
+        self.entries = {}
+
+    def report_many(self, counts, frame):
+        """scheduler.py:60-72."""
+        for key, c in counts.items():
+            e = self.entries.get(key)
+            if e is None:
+                self.entries[key] = [frame, c - 1]
+            else:
+                e[1] += c
+
+    def reinsert(self, keys, frame):
+        for k in keys:
+            self.entries[k] = [frame, 0]
+
+    def select(self, n, exclude):
+        """scheduler.py:79-101: sort, pop in order, excluded deleted not returned."""
+        clamp = self.cfg.rank_clamp
+        if self.cfg.ranking:
+            order = sorted(self.entries.items(), key=lambda kv: (-min(kv[1][0] + kv[1][1], kv[1][0] + clamp), kv[0][1], kv[0][0]))
+        else:
+            order = sorted(self.entries.items(), key=lambda kv: (kv[1][0], kv[0][1], kv[0][0]))
+        picked = []
+        for key, _ in order:
+            if len(picked) == n:
+                break
+            del self.entries[key]
+            if exclude(key):
+                continue
+            picked.append(key)
+        return picked
+
+
+@dataclass
+class Record:
+    """session.py:40-51 FrameRecord."""
+    frame: int
+    wall_s: float
+    fps: float
+    samples: int
+    true_misses: int
+    fallback_hits: int
+    exact_hits: int
+    occupancy: float
+    bricks_loaded: int
+    bricks_loaded_total: int
+    requests_inflight: int
+
+
+class OracleSession:
+    """session.py:54-152 RenderSession (raymarch mode, inline loader, P12)."""
+
+    def __init__(self, field_obj, tf_points, cfg: Config, macro_minmax_arrays=None):
+        self.field = field_obj
+        self.cfg = cfg
+        self.dims = tuple(cfg.dims)
+        if macro_minmax_arrays is None:
+            macro_minmax_arrays = macro_minmax(field_obj.lattice_values(), cfg.macro_cell)
+        self.vmin, self.vmax = macro_minmax_arrays
+        self.set_tf(tf_points)
+        self.cache = OracleCache(cfg) if cfg.cached else None
+        self.req = OracleRequests(self.cache, cfg) if cfg.cached else None
+        self.staged = []
+        self.in_flight = set()
+        self.frame = 0
+        self.camera = None
+        self.last_reports = {}
+        self.last_batch = []
+
+    def set_tf(self, points):
+        """session.py:82-84 -> macrocell.update_majorants."""
+        self.tf_points = np.asarray(points, dtype=np.float64)
+        self.mu = majorants(self.tf_points, self.vmin, self.vmax)
+        self.lut = tf_lut(self.tf_points)
+
+    def set_camera(self, position, target, up=(0.0, 1.0, 0.0), fov_y=45.0, width=256, height=256):
+        self.camera = (tuple(position), tuple(target), tuple(up), fov_y, width, height)
+
+    def reset_cache(self):
+        """session.py:93-101 (P11: session frame -> 0, cache frame kept)."""
+        if self.cache is not None:
+            self.cache.reset()
+            self.req = OracleRequests(self.cache, self.cfg)
+            self.staged = []
+            self.in_flight = set()
+        self.frame = 0
+
+    # ---- sampler (sampler.py:157-280)
+    def _begin_frame(self):
+        pos = np.asarray(self.camera[0], dtype=np.float64)
+        if self.cache is not None:
+            force = (self.cache.max_lod + 1.0) / max(dist_to_unit_box(pos), 1e-6)
+            self.scale = effective_scale(self.cfg.lod_scale, self.cfg.preload, self.frame, force)
+        else:
+            self.scale = self.cfg.lod_scale
+        self.rng = None
+        self.samples = 0
+        self.true_misses = 0
+        self.fallback_hits = 0
+
+    def _sample(self, pos, tmid):
+        n = pos.shape[0]
+        if self.rng is None:
+            self.rng = lane_seeds(self.cfg.seed, self.frame, n)
+        elif self.rng.shape[0] < n:
+            raise AssertionError("lane pool outgrown (never happens in ray-march)")
+        if self.cache is None:
+            vals = np.zeros(n, dtype=np.float32)
+            self.samples += n
+            self.true_misses += n
+            vals[:] = self.field.sample(np.clip(pos, 0.0, np.nextafter(1.0, 0.0)))
+            return vals
+        c = self.cache
+        mode = {"corrected": 0, "as_printed": 1, "off": 2}[self.cfg.mode]
+        if c.paged:
+            # sampler.py:131-142 numpy path: distance = |pos - cam| (P4)
+            dist = np.linalg.norm(pos - np.asarray(self.camera[0], dtype=np.float64), axis=1)
+        else:
+            dist = np.ascontiguousarray(tmid)
+        u = xorshift_uniform(self.rng, n) if mode != 2 else np.zeros(n)
+        vals = np.empty(n, dtype=np.float32)
+        served = np.empty(n, dtype=np.int8)
+        req = np.empty(n, dtype=np.int8)
+        vx, vy, vz = self.dims
+        ex, fb, ms = probe_pass(pos, dist, u, self.scale, mode, float(vx), float(vy), float(vz), c.max_lod, c.b,
+                                c.table, c.offsets, c.grids_arr, c.pool, c.last_used, c.frame, vals, served, req)
+        c.stats["requests"] += n
+        c.stats["exact"] += ex
+        c.stats["fallback"] += fb
+        c.stats["miss"] += ms
+        self.samples += n
+        self.true_misses += ms
+        self.fallback_hits = c.stats["fallback"]
+        if fb or ms:
+            rows = np.flatnonzero(served != req)
+            nat = pos[rows] * np.asarray(self.dims, dtype=np.float64) - 0.5
+            np.clip(nat, 0.0, np.asarray(self.dims, dtype=np.float64) - 1.0, out=nat)
+            c.record_misses(nat, req[rows].astype(np.int64))
+        if ms:
+            mr = np.flatnonzero(served < 0)
+            vals[mr] = self.field.sample(np.clip(pos[mr], 0.0, np.nextafter(1.0, 0.0)))
+        return vals
+
+    # ---- render/raymarch.py:25-120
+    def _raymarch(self):
+        cfg = self.cfg
+        position, target, up, fov, W, H = self.camera
+        self._begin_frame()
+        rot, tan_h, tan_v = camera_setup(position, target, up, fov, W, H)
+        base = film_coords(W, H)
+        n = base.shape[0]
+        origin = np.asarray(position, dtype=np.float64)
+        dirs = np.empty((n, 3)); t0 = np.empty(n); t1 = np.empty(n); keep = np.empty(n, dtype=np.bool_)
+        raygen_pass(base, rot, origin, tan_h, tan_v, dirs, t0, t1, keep)
+        sel = np.flatnonzero(keep)
+        bg = np.asarray(cfg.background, dtype=np.float64)
+        out_rgb = np.broadcast_to(bg, (n, 3)).copy()
+        out_a = np.zeros(n)
+        m = sel.size
+        if m:
+            vx, vy, vz = self.dims
+            dt_base = cfg.base_step_scale * float(np.linalg.norm([1.0 / vx, 1.0 / vy, 1.0 / vz]))
+            cell = cfg.macro_cell
+            cw = (cell / vx, cell / vy, cell / vz)
+            gz, gy, gx = self.mu.shape
+            mu_flat = np.ascontiguousarray(self.mu.ravel())
+            o = np.empty((m, 3)); o[:] = origin
+            d = np.ascontiguousarray(dirs[sel]); t_en = t0[sel].copy(); t_ex = t1[sel].copy()
+            color = np.zeros((m, 3)); trans = np.ones(m)
+            cur_f = t_en.copy(); cur_k = np.zeros(m, dtype=np.int64)
+            active = np.ones(m, dtype=np.bool_)
+            pbuf = np.empty((m, 3)); dtb = np.empty(m); tmb = np.empty(m)
+            smask = np.empty(m, dtype=np.bool_); dmask = np.empty(m, dtype=np.bool_)
+            for _ in range(cfg.max_iterations):
+                advance_pass(o, d, t_en, t_ex, cur_f, cur_k, active, cfg.adaptive, cfg.skip_empty, dt_base,
+                             cfg.mu_floor, mu_flat, gx, gy, gz, cw[0], cw[1], cw[2], pbuf, dtb, tmb, smask, dmask)
+                active &= ~dmask
+                rows = np.flatnonzero(smask)
+                if rows.size:
+                    vals = self._sample(np.ascontiguousarray(pbuf[rows]), tmb[rows])
+                    dead = np.zeros(rows.size, dtype=np.bool_)
+                    shade_pass(rows, np.ascontiguousarray(vals, dtype=np.float32), np.ascontiguousarray(dtb[rows]),
+                               self.lut, cfg.adaptive, dt_base, cfg.term, color, trans, dead)
+                    active[rows[dead]] = False
+                if not active.any():
+                    break
+            out_rgb[sel] = color + trans[:, None] * bg
+            out_a[sel] = 1.0 - trans
+        img = np.concatenate([out_rgb, out_a[:, None]], axis=1).astype(np.float32)
+        return img.reshape(H, W, 4)
+
+    def _maintenance(self):
+        """session.py:132-142 with InlineLoader (scheduler.py:137-172)."""
+        c = self.cache
+        if c is None:
+            return 0
+        reports, c.miss = c.miss, {}
+        self.last_reports = reports
+        self.req.report_many(reports, self.frame)
+        loaded = 0
+        done, self.staged = self.staged, []
+        self.in_flight = set()
+        for key, samples in done:
+            if c.insert(key, samples, self.frame) is not None:
+                loaded += 1
+        self.last_batch = []
+        keys = self.req.select(self.cfg.max_requests, lambda k: c.is_mapped(*k) or k in self.in_flight)
+        self.last_batch = keys
+        if keys:
+            self.in_flight = set(keys)
+            try:
+                for key in keys:
+                    _, norm = brick_positions(self.dims, c.b, key[0], c.unlinear(key[0], key[1]))
+                    self.staged.append((key, np.asarray(self.field.sample(norm), dtype=np.float32)))
+            except (ValueError, FloatingPointError):
+                self.req.reinsert(keys, self.frame)
+                self.in_flight = set()
+                self.staged = []
+        return loaded
+
+    def render_frame(self):
+        t0 = time.perf_counter()
+        img = self._raymarch()
+        loaded = self._maintenance()
+        wall = time.perf_counter() - t0
+        c = self.cache
+        rec = Record(self.frame, wall, 1.0 / wall if wall > 0 else float("inf"), self.samples, self.true_misses,
+                     self.fallback_hits, c.stats["exact"] if c else 0, c.occupancy() if c else 0.0, loaded,
+                     c.loaded_total if c else 0, len(self.in_flight) if c else 0)
+        if c is not None:
+            c.tick()
+        self.frame += 1
+        return img, rec
