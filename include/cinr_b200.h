@@ -1,0 +1,220 @@
+/*
+ * cinr_b200.h — C ABI of the B200-native cached-INR ray-march path.
+ *
+ * Plain C structs + device pointers + sizes; no torch types.  Every entry
+ * point returns 0 on success or a negative status, with the message available
+ * from vcb_last_error() (thread-local).  Streams are passed as `void*`
+ * (a cudaStream_t; NULL = legacy default stream).  Callers own all memory.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/voxcache/):
+ *
+ *   Operator ABI (Stage A drop-in: one export per numba pass; the reference
+ *   resolves these module attributes at call time, so a plugin swaps them):
+ *     vcb_raygen_pass   <- render/kernels.py:426 raygen_pass   (_raygen_one 376-411)
+ *     vcb_advance_pass  <- render/kernels.py:160 advance_pass  (_advance_one 35-137)
+ *     vcb_probe_pass    <- render/kernels.py:316 probe_pass    (_probe_one 166-273)
+ *     vcb_shade_pass    <- render/kernels.py:370 shade_pass    (_shade_one 322-355)
+ *   Field / decoder ABI (the Field.sample_batch duck type, fields.py:89-97):
+ *     vcb_field_points  <- InrField/RawLatticeField/ProceduralField.sample_batch
+ *                          (inr/model.py:65-89, encoding.py:119-134, mlp.py:39-53,
+ *                          fields.py:165-221, fields.py:131-158)
+ *     vcb_field_bricks  <- scheduler.py:127-134 fulfill (+ brickmath.py:125-139
+ *                          sample_positions), written straight into a pool/staging slab
+ *     vcb_macro_minmax  <- macrocell.py:49-74 build (lattice decode + dilated min/max)
+ *   Session ABI (Stage B drop-in: the GPU-resident RenderSession):
+ *     vcb_march_frame   <- render/raymarch.py:25-120 raymarch_frame with the
+ *                          VolumeSampler probe/miss path (sampler.py:196-280)
+ *     vcb_maintenance   <- session.py:132-142 _maintenance: Mrpd.drain_miss_reports
+ *                          (mrpd.py:263), RequestTable.report_many/select_batch
+ *                          (scheduler.py:60-101), InlineLoader collect/dispatch
+ *                          (scheduler.py:137-172), Mrpd.insert + BrickPool.acquire_slot
+ *                          (mrpd.py:229-256, pool.py:55-68)
+ */
+#ifndef CINR_B200_H
+#define CINR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VCB_MAX_LOD 32
+#define VCB_MAX_LEVELS 16
+#define VCB_MAX_LAYERS 8
+
+/* camera.py:129-138: origin, rot = [right, up, fwd] as columns (row-major 3x3),
+ * tan_h = tan(fov/2)*aspect, tan_v = tan(fov/2). */
+typedef struct {
+    double origin[3];
+    double rot[9];
+    double tan_h, tan_v;
+    int32_t width, height;
+} VcbCamera;
+
+/* advance_pass scalars (kernels.py:35-39). gx/gy/gz macro grid, cw* cell widths. */
+typedef struct {
+    int32_t adaptive, skip_empty;
+    double dt_base, mu_floor;
+    int64_t gx, gy, gz;
+    double cwx, cwy, cwz;
+} VcbMarchStatic;
+
+/* probe_pass scalars (kernels.py:166-170) + packed table geometry (mrpd.py:91-114). */
+typedef struct {
+    double vx, vy, vz, lod_scale;
+    int32_t mode;    /* 0 corrected, 1 as_printed, 2 off (sampler.py:233) */
+    int32_t max_lod;
+    int64_t b;       /* brick size */
+    int32_t b_pow2;  /* 1 if every span B<<L is a power of two */
+    int32_t pad_;
+    int64_t grid[VCB_MAX_LOD][3];
+    int64_t offset[VCB_MAX_LOD];
+} VcbProbeStatic;
+
+/* Field descriptor: kind 0 = hash-grid INR, 1 = lattice, 2 = procedural. */
+typedef struct {
+    int32_t kind;
+    /* INR (HashGridConfig / MLPConfig, encoding.py:30-64, mlp.py:13-25) */
+    int32_t levels, feats, out_sigmoid, n_layers;
+    int64_t table_size;
+    int32_t res[VCB_MAX_LEVELS];
+    int32_t dense[VCB_MAX_LEVELS];
+    int64_t tab_off[VCB_MAX_LEVELS];       /* row offset of each level */
+    int32_t widths[VCB_MAX_LAYERS + 1];    /* input, hidden..., 1 */
+    int64_t w_off[VCB_MAX_LAYERS], b_off[VCB_MAX_LAYERS];
+    const float *tables;                   /* [rows][feats] */
+    const float *weights;                  /* packed (out,in) row-major per layer */
+    const float *biases;
+    /* lattice (z,y,x) f32 */
+    const float *lattice;
+    int64_t lx, ly, lz;
+    /* procedural: 0 sphere, 1 shells, 2 marschner_lobb_like (fields.py:131-148) */
+    int32_t proc;
+    int32_t clip01;                        /* InrField clip (model.py:88-89) */
+} VcbField;
+
+/* Brick geometry for decode (brickmath.py:87-139). */
+typedef struct {
+    int64_t dims[3];
+    int64_t b;
+    int32_t n_lod, pad_;
+    int64_t grid[VCB_MAX_LOD][3];
+    int64_t offset[VCB_MAX_LOD];
+} VcbBrickGeom;
+
+/* Per-frame device counters (FrameStats, mrpd.py:33-41 + sampler counters). */
+typedef struct {
+    int64_t requests, exact, fallback, miss;
+    int64_t iterations, rays;
+    int64_t misses_resolved;
+    int64_t nonfinite;      /* true-miss inference produced NaN/Inf (ModelCorruptError) */
+    int64_t pad_[8];
+} VcbFrameStats;
+
+/* Device-resident cache bookkeeping (pool free list, loader, counters). */
+typedef struct {
+    int64_t next_free;      /* free slots are [next_free, S) — pool.py:46,57-58 */
+    int64_t loaded_total;   /* mrpd.py:84-85 */
+    int64_t n_staged;       /* bricks dispatched last maintenance (InlineLoader._staged) */
+    int64_t staged_frame;
+    int64_t decode_error;   /* non-finite decode -> reinsert (scheduler.py:164-168) */
+    int64_t bricks_loaded;  /* this maintenance */
+    int64_t deferred, inserted;
+    int64_t n_inflight;
+    int64_t n_reports, n_pending, n_batch;
+    int64_t pad_[4];
+} VcbCacheState;
+
+typedef struct {
+    VcbCamera cam;
+    VcbMarchStatic adv;
+    VcbProbeStatic probe;
+    int32_t cached;          /* 0 = uncached baseline (session.py:63-70) */
+    int32_t paged_dist;      /* 1 = |pos-cam| distances (sampler.py:135 numpy path) */
+    int64_t cache_frame;     /* probe stamp clock (P11) */
+    uint64_t rng_base;       /* splitmix64(seed ^ frame*GOLDEN), sampler.py:41 */
+    double term;
+    double bg[3];
+    int32_t lut_size;
+    int32_t max_iterations;
+    uint32_t epoch;          /* monotonic per call; tags look-back status words */
+    int32_t pad_;
+    const float *mu;         /* majorants [gz][gy][gx] */
+    const float *lut;        /* [lut_size][4] */
+    const int32_t *table;    /* dense logical MRPD, all LoDs */
+    const float *pool;       /* [S][B][B][B] */
+    int64_t *last_used;      /* [S] */
+    int32_t *miss_count;     /* per brick, all LoDs */
+    VcbField field;          /* true-miss inference */
+    float *image;            /* [H][W][4] */
+    VcbFrameStats *stats;    /* device */
+    void *workspace;
+    int64_t workspace_bytes;
+    int64_t reserved_;
+} VcbFrameParams;
+
+typedef struct {
+    VcbBrickGeom geom;
+    int64_t total;           /* bricks over all LoDs */
+    int64_t slots;
+    int64_t session_frame;
+    int32_t max_requests, ranking;
+    int64_t rank_clamp;
+    int32_t lin_bits, lod_bits;
+    int32_t *table;
+    float *pool;
+    int64_t *owner;          /* [S] flat brick id or -1 */
+    int64_t *last_used;
+    int32_t *miss_count;
+    int64_t *req_base;       /* -1 absent */
+    int64_t *req_hits;
+    VcbCacheState *state;
+    float *staging;          /* [max_requests][B^3] */
+    int64_t *staged_keys;    /* [max_requests] flat brick ids in batch order */
+    void *workspace;
+    int64_t workspace_bytes;
+    int64_t *dbg_reports;    /* optional [total][2] (flat id, count), NULL to skip */
+    VcbField field;
+} VcbMaintParams;
+
+const char *vcb_last_error(void);
+int32_t vcb_abi_version(void);
+int32_t vcb_device_sm_count(void);
+/* host-only: sizeof of VcbCamera, VcbMarchStatic, VcbProbeStatic, VcbField, VcbBrickGeom,
+ * VcbFrameStats, VcbCacheState, VcbFrameParams, VcbMaintParams (ABI self-check) */
+int32_t vcb_struct_sizes(int64_t *out, int32_t n);
+
+/* ---- operator ABI (device pointers, row-major arrays as in kernels.py) */
+int32_t vcb_raygen_pass(int64_t n, const double *base_dirs, const double *rot, const double *origin, double tan_h,
+                        double tan_v, double *dirs, double *t0, double *t1, uint8_t *keep, void *stream);
+int32_t vcb_advance_pass(int64_t n, const double *o, const double *d, const double *t_en, const double *t_ex,
+                         double *cursor_f, int64_t *cursor_k, const uint8_t *active, const VcbMarchStatic *s,
+                         const float *mu, double *out_pos, double *out_dt, double *out_tmid, uint8_t *sample_mask,
+                         uint8_t *done_mask, void *stream);
+int32_t vcb_probe_pass(int64_t n, const double *pos, const double *dist, const double *u, const VcbProbeStatic *p,
+                       const int32_t *table, const float *pool, int64_t *last_used, int64_t frame, float *values,
+                       int8_t *served, int8_t *req, int64_t *counts /* device [3] */, void *stream);
+int32_t vcb_shade_pass(int64_t n, const int64_t *rows, const float *values, const double *dt, const float *lut,
+                       int64_t lut_size, int32_t adaptive, double dt_base, double term, double *color, double *trans,
+                       uint8_t *dead, void *stream);
+
+/* ---- field / decoder ABI */
+int32_t vcb_field_points(const VcbField *f, int64_t n, const double *pos, float *out, int32_t *nonfinite,
+                         void *stream);
+int32_t vcb_field_bricks(const VcbField *f, const VcbBrickGeom *g, int64_t n_keys, const int64_t *keys,
+                         float *out, int32_t *nonfinite, void *stream);
+int32_t vcb_macro_minmax(const VcbField *f, const int64_t *dims, int64_t cell, float *vmin, float *vmax,
+                         void *stream);
+
+/* ---- session ABI */
+int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);
+int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);
+int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests);
+int32_t vcb_maintenance(const VcbMaintParams *p, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,166 @@
+"""ctypes binding of the C ABI in include/cinr_b200.h (libcinr_b200.so).
+
+There is no fallback: if the library cannot be loaded, every GPU entry point
+raises NativeUnavailable.  Struct layouts mirror the header field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import VoxcacheError
+
+MAX_LOD = 32
+MAX_LEVELS = 16
+MAX_LAYERS = 8
+
+_LIB = None
+_SO = Path(__file__).resolve().parent / "_lib" / "libcinr_b200.so"
+
+
+class NativeUnavailable(VoxcacheError):
+    """The sm_100a library is missing or failed to load (no CPU fallback exists)."""
+
+
+class NativeError(VoxcacheError):
+    """A C-ABI call returned a non-zero status."""
+
+
+i64 = C.c_int64
+i32 = C.c_int32
+f64 = C.c_double
+vp = C.c_void_p
+
+
+class VcbCamera(C.Structure):
+    _fields_ = [("origin", f64 * 3), ("rot", f64 * 9), ("tan_h", f64), ("tan_v", f64), ("width", i32), ("height", i32)]
+
+
+class VcbMarchStatic(C.Structure):
+    _fields_ = [("adaptive", i32), ("skip_empty", i32), ("dt_base", f64), ("mu_floor", f64),
+                ("gx", i64), ("gy", i64), ("gz", i64), ("cwx", f64), ("cwy", f64), ("cwz", f64)]
+
+
+class VcbProbeStatic(C.Structure):
+    _fields_ = [("vx", f64), ("vy", f64), ("vz", f64), ("lod_scale", f64), ("mode", i32), ("max_lod", i32),
+                ("b", i64), ("b_pow2", i32), ("pad_", i32), ("grid", (i64 * 3) * MAX_LOD), ("offset", i64 * MAX_LOD)]
+
+
+class VcbField(C.Structure):
+    _fields_ = [("kind", i32), ("levels", i32), ("feats", i32), ("out_sigmoid", i32), ("n_layers", i32),
+                ("table_size", i64), ("res", i32 * MAX_LEVELS), ("dense", i32 * MAX_LEVELS),
+                ("tab_off", i64 * MAX_LEVELS), ("widths", i32 * (MAX_LAYERS + 1)),
+                ("w_off", i64 * MAX_LAYERS), ("b_off", i64 * MAX_LAYERS),
+                ("tables", vp), ("weights", vp), ("biases", vp),
+                ("lattice", vp), ("lx", i64), ("ly", i64), ("lz", i64), ("proc", i32), ("clip01", i32)]
+
+
+class VcbBrickGeom(C.Structure):
+    _fields_ = [("dims", i64 * 3), ("b", i64), ("n_lod", i32), ("pad_", i32), ("grid", (i64 * 3) * MAX_LOD),
+                ("offset", i64 * MAX_LOD)]
+
+
+class VcbFrameStats(C.Structure):
+    _fields_ = [("requests", i64), ("exact", i64), ("fallback", i64), ("miss", i64), ("iterations", i64),
+                ("rays", i64), ("misses_resolved", i64), ("nonfinite", i64), ("pad_", i64 * 8)]
+
+
+class VcbCacheState(C.Structure):
+    _fields_ = [("next_free", i64), ("loaded_total", i64), ("n_staged", i64), ("staged_frame", i64),
+                ("decode_error", i64), ("bricks_loaded", i64), ("deferred", i64), ("inserted", i64),
+                ("n_inflight", i64), ("n_reports", i64), ("n_pending", i64), ("n_batch", i64), ("pad_", i64 * 4)]
+
+
+class VcbFrameParams(C.Structure):
+    _fields_ = [("cam", VcbCamera), ("adv", VcbMarchStatic), ("probe", VcbProbeStatic), ("cached", i32),
+                ("paged_dist", i32), ("cache_frame", i64), ("rng_base", C.c_uint64), ("term", f64), ("bg", f64 * 3),
+                ("lut_size", i32), ("max_iterations", i32), ("epoch", C.c_uint32), ("pad_", i32),
+                ("mu", vp), ("lut", vp), ("table", vp), ("pool", vp), ("last_used", vp), ("miss_count", vp),
+                ("field", VcbField), ("image", vp), ("stats", vp), ("workspace", vp), ("workspace_bytes", i64),
+                ("reserved_", i64)]
+
+
+class VcbMaintParams(C.Structure):
+    _fields_ = [("geom", VcbBrickGeom), ("total", i64), ("slots", i64), ("session_frame", i64),
+                ("max_requests", i32), ("ranking", i32), ("rank_clamp", i64), ("lin_bits", i32), ("lod_bits", i32),
+                ("table", vp), ("pool", vp), ("owner", vp), ("last_used", vp), ("miss_count", vp),
+                ("req_base", vp), ("req_hits", vp), ("state", vp), ("staging", vp), ("staged_keys", vp),
+                ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField)]
+
+
+_PROTOS = {
+    "vcb_last_error": (C.c_char_p, []),
+    "vcb_abi_version": (i32, []),
+    "vcb_device_sm_count": (i32, []),
+    "vcb_struct_sizes": (i32, [vp, i32]),
+    "vcb_raygen_pass": (i32, [i64, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp]),
+    "vcb_advance_pass": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, C.POINTER(VcbMarchStatic), vp, vp, vp, vp, vp, vp, vp]),
+    "vcb_probe_pass": (i32, [i64, vp, vp, vp, C.POINTER(VcbProbeStatic), vp, vp, vp, i64, vp, vp, vp, vp, vp]),
+    "vcb_shade_pass": (i32, [i64, vp, vp, vp, vp, i64, i32, f64, f64, vp, vp, vp, vp]),
+    "vcb_field_points": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),
+    "vcb_field_bricks": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
+    "vcb_macro_minmax": (i32, [C.POINTER(VcbField), vp, i64, vp, vp, vp]),
+    "vcb_frame_workspace_bytes": (i64, [i64, i32]),
+    "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),
+    "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
+    "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
+}
+
+EXPORTS = tuple(_PROTOS)
+
+
+def library_path() -> Path:
+    return _SO
+
+
+def load():
+    """Load (building in-tree first when sources are newer) the sm_100a library."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    try:
+        from . import _build
+
+        if _build.needs_build():
+            _build.build()
+    except Exception as exc:  # a missing nvcc on a prebuilt tree is fine
+        if not _SO.exists():
+            raise NativeUnavailable(f"cannot build {_SO.name}: {exc}") from exc
+    if not _SO.exists():
+        raise NativeUnavailable(f"{_SO} not built (run __graft_entry__.build())")
+    try:
+        lib = C.CDLL(str(_SO))
+    except OSError as exc:
+        raise NativeUnavailable(f"cannot load {_SO}: {exc}") from exc
+    for name, (res, args) in _PROTOS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+STRUCTS = (VcbCamera, VcbMarchStatic, VcbProbeStatic, VcbField, VcbBrickGeom, VcbFrameStats, VcbCacheState,
+           VcbFrameParams, VcbMaintParams)
+
+
+def struct_sizes():
+    """(python sizeof, C sizeof) per ABI struct; host-only call, no GPU needed."""
+    import numpy as np
+
+    out = np.zeros(16, dtype=np.int64)
+    n = load().vcb_struct_sizes(out.ctypes.data, 16)
+    return [(s.__name__, C.sizeof(s), int(out[i])) for i, s in enumerate(STRUCTS[:n])]
+
+
+def check(rc: int, what: str = ""):
+    if rc != 0:
+        msg = load().vcb_last_error().decode(errors="replace")
+        raise NativeError(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc

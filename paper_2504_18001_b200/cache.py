@@ -1,0 +1,325 @@
+"""Multi-resolution page table (MRPD), brick pool and request table on the device.
+
+Host side: brick geometry (voxcache/cache/brickmath.py:25-151) and configs
+(mrpd.py:21-29, pool.py:15-33).  Device side (`DeviceCache`): one dense int32
+residency table over every LoD (the logical view of DirectTable/PagedTable,
+P13; 4096^3@B16 is 78 MB, trivial in 180 GB HBM), the f32 pool [S][B][B][B],
+owner/last_used per slot, per-brick miss counters and the request table as
+per-brick (base, hits) arrays.  All mutation happens in the maintenance
+kernels (csrc/cache.cu); the host only reads state back for diagnostics.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import ptr, stream_ptr
+
+
+# ----------------------------------------------------------------- brick math
+def lod_stride(lod: int) -> int:
+    return 1 << lod
+
+
+def brick_span(brick_size: int, lod: int) -> int:
+    return brick_size << lod
+
+
+def brick_origin(index, brick_size: int, lod: int):
+    """k*B*2^L - 1 for k > 0, 0 for k = 0 (brickmath.py:35-39; P1)."""
+    index = np.asarray(index, dtype=np.int64)
+    o = index * brick_span(brick_size, lod)
+    return np.where(index > 0, o - 1, o)
+
+
+def locate_axis(position, brick_size: int, lod: int):
+    return np.floor((np.asarray(position, dtype=np.float64) + 1.0) / brick_span(brick_size, lod)).astype(np.int64)
+
+
+def grid_dims_axis(voxels: int, brick_size: int, lod: int) -> int:
+    s = lod_stride(lod)
+    if voxels <= (brick_size - 1) * s + 1:
+        return 1
+    return int(-(-(voxels + s) // brick_span(brick_size, lod)))
+
+
+def grid_dims(dims, brick_size: int, lod: int):
+    return tuple(grid_dims_axis(v, brick_size, lod) for v in dims)
+
+
+def max_lod(dims, brick_size: int) -> int:
+    lod = 0
+    while grid_dims(dims, brick_size, lod) != (1, 1, 1):
+        lod += 1
+        if lod > 48:
+            raise ValueError(f"no single-brick LoD for dims {dims} at brick size {brick_size}")
+    return lod
+
+
+@dataclass(frozen=True)
+class BrickKey:
+    lod: int
+    index: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "index", tuple(int(i) for i in self.index))
+
+    def linear_index(self, grid) -> int:
+        i, j, k = self.index
+        return i + grid[0] * (j + grid[1] * k)
+
+
+class BrickLayout:
+    """brickmath.py:87-151."""
+
+    def __init__(self, dims, brick_size: int):
+        if brick_size < 2:
+            raise ValueError("brick_size must be >= 2")
+        self.dims = tuple(int(d) for d in dims)
+        self.brick_size = int(brick_size)
+        self.max_lod = max_lod(self.dims, self.brick_size)
+        self.grids = [grid_dims(self.dims, self.brick_size, l) for l in range(self.max_lod + 1)]
+        counts = [g[0] * g[1] * g[2] for g in self.grids]
+        self.offsets = [int(v) for v in np.concatenate([[0], np.cumsum(counts)[:-1]])]
+        self.total = int(sum(counts))
+
+    def brick_count(self, lod: int) -> int:
+        g = self.grids[lod]
+        return g[0] * g[1] * g[2]
+
+    def total_bricks(self) -> int:
+        return self.total
+
+    def flat(self, key: BrickKey) -> int:
+        return self.offsets[key.lod] + key.linear_index(self.grids[key.lod])
+
+    def key_of_flat(self, flat: int) -> BrickKey:
+        lod = int(np.searchsorted(self.offsets, flat, side="right") - 1)
+        lin = flat - self.offsets[lod]
+        g = self.grids[lod]
+        return BrickKey(lod, (lin % g[0], (lin // g[0]) % g[1], lin // (g[0] * g[1])))
+
+    def locate(self, positions, lod: int):
+        if lod > self.max_lod:
+            raise ValueError(f"lod {lod} exceeds max_lod {self.max_lod}")
+        pos = np.asarray(positions, dtype=np.float64)
+        idx = locate_axis(pos, self.brick_size, lod)
+        np.clip(idx, 0, np.asarray(self.grids[lod], dtype=np.int64) - 1, out=idx)
+        local = (pos - brick_origin(idx, self.brick_size, lod)) / lod_stride(lod)
+        np.clip(local, 0.0, self.brick_size - 1, out=local)
+        return idx, local
+
+    def origin(self, key: BrickKey):
+        return tuple(int(v) for v in brick_origin(np.asarray(key.index), self.brick_size, key.lod))
+
+    def sample_positions(self, key: BrickKey):
+        b = self.brick_size
+        axis = np.arange(b, dtype=np.int64) * lod_stride(key.lod)
+        zz, yy, xx = np.meshgrid(axis, axis, axis, indexing="ij")
+        native = np.stack([xx.ravel(), yy.ravel(), zz.ravel()], axis=1) + np.asarray(self.origin(key))
+        np.clip(native, 0, np.asarray(self.dims, dtype=np.int64) - 1, out=native)
+        return native, (native + 0.5) / np.asarray(self.dims, dtype=np.float64)
+
+    def keys_at(self, lod: int):
+        gx, gy, gz = self.grids[lod]
+        for k in range(gz):
+            for j in range(gy):
+                for i in range(gx):
+                    yield BrickKey(lod, (i, j, k))
+
+    def valid_key(self, key: BrickKey) -> bool:
+        if not 0 <= key.lod <= self.max_lod:
+            return False
+        return all(0 <= key.index[a] < self.grids[key.lod][a] for a in range(3))
+
+    def geom(self) -> N.VcbBrickGeom:
+        g = N.VcbBrickGeom()
+        for a in range(3):
+            g.dims[a] = self.dims[a]
+        g.b = self.brick_size
+        g.n_lod = self.max_lod + 1
+        for l, gr in enumerate(self.grids):
+            for a in range(3):
+                g.grid[l][a] = gr[a]
+            g.offset[l] = self.offsets[l]
+        return g
+
+
+@dataclass(frozen=True)
+class PoolSpec:
+    """pool.py:15-33."""
+
+    pool_dims: tuple
+    brick_size: int
+
+    @property
+    def slot_count(self) -> int:
+        px, py, pz = self.pool_dims
+        return px * py * pz
+
+    @property
+    def voxel_count(self) -> int:
+        return self.slot_count * self.brick_size ** 3
+
+    @property
+    def byte_size(self) -> int:
+        return self.voxel_count * 4
+
+
+@dataclass(frozen=True)
+class CacheConfig:
+    """mrpd.py:21-29."""
+
+    brick_size: int = 40
+    pool_dims: tuple = (8, 8, 8)
+    direct_table_threshold: int = 1 << 18
+    page_size: int = 4096
+    page_budget: int = 64
+
+    def pool_spec(self) -> PoolSpec:
+        return PoolSpec(tuple(self.pool_dims), self.brick_size)
+
+
+def _bits(v: int) -> int:
+    return max(1, int(v).bit_length())
+
+
+class DeviceCache:
+    """GPU-resident Mrpd + BrickPool + RequestTable + InlineLoader staging."""
+
+    def __init__(self, dims, config: CacheConfig, sched, device, debug=False):
+        self.config = config
+        self.sched = sched
+        self.device = device
+        self.layout = BrickLayout(dims, config.brick_size)
+        lay = self.layout
+        if lay.max_lod > 127:
+            raise ValueError("LoD arrays are int8 (P17)")
+        self.max_lod = lay.max_lod
+        counts = [lay.brick_count(l) for l in range(lay.max_lod + 1)]
+        # the reference takes its numpy lookup path (|pos-cam| LoD distances) as
+        # soon as one LoD table is virtualised (mrpd.py:99-100, sampler.py:131-142)
+        self.paged = any(c > config.direct_table_threshold for c in counts)
+        self.slots = config.pool_spec().slot_count
+        b3 = config.brick_size ** 3
+        self.geom = lay.geom()
+        mr = int(sched.max_requests)
+        if mr < 1:
+            raise ValueError("batch size must be >= 1")
+        t = lambda n, dt, fill: torch.full((n,), fill, dtype=dt, device=device)
+        self.table = t(lay.total, torch.int32, -1)
+        self.pool = torch.zeros(self.slots * b3, dtype=torch.float32, device=device)
+        self.owner = t(self.slots, torch.int64, -1)
+        self.last_used = t(self.slots, torch.int64, -1)
+        self.miss_count = t(lay.total, torch.int32, 0)
+        self.req_base = t(lay.total, torch.int64, -1)
+        self.req_hits = t(lay.total, torch.int64, 0)
+        self.state = torch.zeros(C.sizeof(N.VcbCacheState) // 8, dtype=torch.int64, device=device)
+        self.staging = torch.zeros(mr * b3, dtype=torch.float32, device=device)
+        self.staged_keys = t(mr, torch.int64, -1)
+        wsb = N.load().vcb_maint_workspace_bytes(lay.total, self.slots, mr)
+        self.workspace = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.dbg_reports = t(2 * lay.total, torch.int64, 0) if debug else None
+        self.frame = 0  # Mrpd.frame: the probe stamp clock (P11)
+        max_lin = max(counts) - 1
+        self.lin_bits = _bits(max_lin)
+        self.lod_bits = _bits(lay.max_lod)
+        if 63 - self.lin_bits - self.lod_bits < 24:
+            raise ValueError("brick grid too large for 64-bit request keys")
+
+    def reset(self):
+        """mrpd.py:268-276 (Mrpd.frame survives; in-flight loads dropped)."""
+        self.table.fill_(-1)
+        self.pool.zero_()
+        self.owner.fill_(-1)
+        self.last_used.fill_(-1)
+        self.miss_count.zero_()
+        self.req_base.fill_(-1)
+        self.req_hits.zero_()
+        self.state.zero_()
+
+    def maint_params(self, session_frame: int, field_desc) -> N.VcbMaintParams:
+        p = N.VcbMaintParams()
+        p.geom = self.geom
+        p.total = self.layout.total
+        p.slots = self.slots
+        p.session_frame = session_frame
+        p.max_requests = self.sched.max_requests
+        p.ranking = 1 if self.sched.ranking_enabled else 0
+        p.rank_clamp = self.sched.rank_clamp
+        p.lin_bits = self.lin_bits
+        p.lod_bits = self.lod_bits
+        p.table = ptr(self.table)
+        p.pool = ptr(self.pool)
+        p.owner = ptr(self.owner)
+        p.last_used = ptr(self.last_used)
+        p.miss_count = ptr(self.miss_count)
+        p.req_base = ptr(self.req_base)
+        p.req_hits = ptr(self.req_hits)
+        p.state = ptr(self.state)
+        p.staging = ptr(self.staging)
+        p.staged_keys = ptr(self.staged_keys)
+        p.workspace = ptr(self.workspace)
+        p.workspace_bytes = self.workspace.numel()
+        p.dbg_reports = ptr(self.dbg_reports)
+        p.field = field_desc
+        return p
+
+    def maintenance(self, session_frame: int, field_desc, stream=None):
+        p = self.maint_params(session_frame, field_desc)
+        N.call("vcb_maintenance", C.byref(p), stream_ptr(stream))
+
+    # ---- diagnostics (D2H; not on the hot path)
+    def state_dict(self):
+        s = self.state.cpu().numpy()
+        names = [f[0] for f in N.VcbCacheState._fields_ if f[0] != "pad_"]
+        return {n: int(s[i]) for i, n in enumerate(names)}
+
+    def occupancy_from(self, st) -> float:
+        return 1.0 - (self.slots - st["next_free"]) / self.slots
+
+    def is_mapped(self, key: BrickKey) -> bool:
+        return int(self.table[self.layout.flat(key)].item()) >= 0
+
+    def dump(self):
+        """Reference-shaped state: dense tables, owner (lod, linear), stamps, requests."""
+        lay = self.layout
+        offs = np.asarray(lay.offsets, dtype=np.int64)
+        own = self.owner.cpu().numpy()
+        pairs = np.full((self.slots, 2), -1, dtype=np.int64)
+        m = own >= 0
+        lods = np.searchsorted(offs, own[m], side="right") - 1
+        pairs[m, 0] = lods
+        pairs[m, 1] = own[m] - offs[lods]
+        base = self.req_base.cpu().numpy()
+        hits = self.req_hits.cpu().numpy()
+        pend = np.flatnonzero(base >= 0)
+        pl = np.searchsorted(offs, pend, side="right") - 1
+        ents = np.stack([pl, pend - offs[pl], base[pend], hits[pend]], axis=1) if pend.size else np.zeros((0, 4), np.int64)
+        ents = ents[np.lexsort((ents[:, 1], ents[:, 0]))] if pend.size else ents
+        st = self.state_dict()
+        return dict(tables=self.table.cpu().numpy(), owner=pairs, last_used=self.last_used.cpu().numpy(),
+                    n_free=self.slots - st["next_free"], cache_frame=self.frame, entries=ents.astype(np.int64),
+                    state=st)
+
+    def batch(self):
+        st = self.state_dict()
+        keys = self.staged_keys[: st["n_batch"]].cpu().numpy()
+        offs = np.asarray(self.layout.offsets, dtype=np.int64)
+        l = np.searchsorted(offs, keys, side="right") - 1
+        return np.stack([l, keys - offs[l]], axis=1).astype(np.int64).reshape(-1, 2)
+
+    def reports(self):
+        st = self.state_dict()
+        if self.dbg_reports is None:
+            return None
+        r = self.dbg_reports[: 2 * st["n_reports"]].cpu().numpy().reshape(-1, 2)
+        offs = np.asarray(self.layout.offsets, dtype=np.int64)
+        l = np.searchsorted(offs, r[:, 0], side="right") - 1
+        out = np.stack([l, r[:, 0] - offs[l], r[:, 1]], axis=1).astype(np.int64)
+        return out[np.lexsort((out[:, 1], out[:, 0]))].reshape(-1, 3)

@@ -1,0 +1,417 @@
+// Between-frame maintenance on device (session.py:132-142), bit-exact with the
+// reference's single-writer Python logic:
+//   k_report      Mrpd.drain_miss_reports + RequestTable.report_many
+//                 (mrpd.py:263-266, scheduler.py:60-72): new key -> base=f,
+//                 hits=c-1; existing -> hits+=c (order-independent)
+//   k_insert      InlineLoader.collect + Mrpd.insert (mrpd.py:229-256) with
+//                 BrickPool.acquire_slot (pool.py:55-62): free slots ascending,
+//                 then argmin(last_used) over last_used < f, lowest slot on ties,
+//                 else deferred; the LRU picks of one batch are the m smallest
+//                 (last_used, slot) keys, found by a block radix select
+//   k_pending +   RequestTable.select_batch (scheduler.py:79-101): composite
+//   k_select      64-bit key (-rank|base, linear, lod); the smallest prefix holding
+//                 n non-excluded (mapped) entries is deleted, its non-excluded
+//                 entries returned in key order
+//   field decode  fulfill (scheduler.py:127-134) into the staging slab; a
+//                 non-finite decode re-enters the keys with base=f (164-168)
+#include <cstddef>
+
+#include "common.cuh"
+#include "fields.cuh"
+#include "util.cuh"
+
+namespace cinr {
+
+constexpr int kSelThreads = 1024;
+constexpr int kMaxSel = 2048;  // max_requests bound for the in-CTA selection
+
+struct MaintWs {
+    long long* pend_key;   // [total]
+    long long* pend_flat;  // [total]
+    int* ctr;              // [0] n_pending, [1] n_reports
+    long long* lru;        // [kMaxSel]
+    int* assign;           // [kMaxSel]
+    int* nonfinite;
+};
+
+inline int64_t maint_ws_layout(int64_t total, void* base, MaintWs* w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = (off + 255) / 256 * 256;
+        off = o + bytes;
+        return o;
+    };
+    size_t a = take((size_t)total * 8), b = take((size_t)total * 8), c = take(64), d = take(kMaxSel * 8),
+           e = take(kMaxSel * 4), f = take(64);
+    if (base && w) {
+        char* p = (char*)base;
+        w->pend_key = (long long*)(p + a);
+        w->pend_flat = (long long*)(p + b);
+        w->ctr = (int*)(p + c);
+        w->lru = (long long*)(p + d);
+        w->assign = (int*)(p + e);
+        w->nonfinite = (int*)(p + f);
+    }
+    return (int64_t)((off + 255) / 256 * 256);
+}
+
+__device__ __forceinline__ int lod_of(const VcbBrickGeom& G, long long flat) {
+    int lod = 0;
+    while (lod + 1 < G.n_lod && flat >= G.offset[lod + 1]) lod++;
+    return lod;
+}
+
+__global__ void k_report(VcbMaintParams P, MaintWs w) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
+         b += (long long)gridDim.x * blockDim.x) {
+        const int c = P.miss_count[b];
+        if (c == 0) continue;
+        P.miss_count[b] = 0;
+        if (P.req_base[b] < 0) {
+            P.req_base[b] = P.session_frame;
+            P.req_hits[b] = c - 1;
+        } else {
+            P.req_hits[b] += c;
+        }
+        const int r = atomicAdd(&w.ctr[1], 1);
+        if (P.dbg_reports) {
+            P.dbg_reports[2 * r] = b;
+            P.dbg_reports[2 * r + 1] = c;
+        }
+    }
+}
+
+// Smallest-m selection of unique 64-bit keys by one CTA: MSB-first radix select
+// with 8-bit digits, then the <= threshold keys are gathered and rank-sorted.
+struct SelSmem {
+    unsigned int hist[256];
+    unsigned long long prefix, mask;
+    long long remaining;
+    int n_out;
+    long long out[kMaxSel];
+};
+
+template <typename KeyFn>
+__device__ int block_select_smallest(KeyFn key_of, long long n, int m, SelSmem& s, long long* sorted_out) {
+    // key_of(i, &k) -> false when element i is not a candidate
+    if (threadIdx.x == 0) {
+        s.prefix = 0;
+        s.mask = 0;
+        s.remaining = m;
+        s.n_out = 0;
+    }
+    // count candidates and find the key bit-width
+    __shared__ unsigned long long kmax_s;
+    __shared__ long long ncand_s;
+    if (threadIdx.x == 0) {
+        kmax_s = 0;
+        ncand_s = 0;
+    }
+    __syncthreads();
+    unsigned long long kmax = 0;
+    long long nc = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        unsigned long long k;
+        if (key_of(i, k)) {
+            kmax = k > kmax ? k : kmax;
+            nc++;
+        }
+    }
+    atomicMax(&kmax_s, kmax);
+    atomicAdd((unsigned long long*)&ncand_s, (unsigned long long)nc);
+    __syncthreads();
+    const long long ncand = ncand_s;
+    unsigned long long thresh = ~0ull;
+    if (ncand > m) {
+        int top = 64 - __clzll((long long)kmax_s);
+        int shift = ((top + 7) / 8) * 8;
+        while (shift > 0) {
+            shift -= 8;
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) s.hist[i] = 0;
+            __syncthreads();
+            const unsigned long long pf = s.prefix, mk = s.mask;
+            for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+                unsigned long long k;
+                if (key_of(i, k) && (k & mk) == pf) atomicAdd(&s.hist[(k >> shift) & 255ull], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long rem = s.remaining;
+                int d = 0;
+                for (; d < 256; d++) {
+                    if ((long long)s.hist[d] >= rem) break;
+                    rem -= s.hist[d];
+                }
+                s.remaining = rem;
+                s.prefix = pf | ((unsigned long long)d << shift);
+                s.mask = mk | (255ull << shift);
+            }
+            __syncthreads();
+        }
+        thresh = s.prefix;  // the m-th smallest key
+    }
+    __syncthreads();
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        unsigned long long k;
+        if (key_of(i, k) && k <= thresh) {
+            int o = atomicAdd(&s.n_out, 1);
+            if (o < kMaxSel) s.out[o] = (long long)k;
+        }
+    }
+    __syncthreads();
+    const int cnt = s.n_out < kMaxSel ? s.n_out : kMaxSel;
+    // rank sort (keys unique)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const long long k = s.out[i];
+        int r = 0;
+        for (int j = 0; j < cnt; j++) r += s.out[j] < k;
+        sorted_out[r] = k;
+    }
+    __syncthreads();
+    return cnt;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_insert(VcbMaintParams P, MaintWs w) {
+    __shared__ SelSmem s;
+    __shared__ long long n_lru_s;
+    VcbCacheState* st = P.state;
+    const long long n = st->n_staged;
+    if (n == 0) {
+        if (threadIdx.x == 0) {
+            st->bricks_loaded = 0;
+            st->deferred = 0;
+            st->inserted = 0;
+        }
+        return;
+    }
+    const long long f = P.session_frame;
+    const long long nf0 = st->next_free;
+    const long long free_left = P.slots - nf0;
+    // LRU candidates only matter when the free list cannot cover the batch
+    long long n_lru = 0;
+    if (n > free_left) {
+        int slot_bits = 1;
+        while ((1ll << slot_bits) < P.slots) slot_bits++;
+        auto key_of = [&](long long i, unsigned long long& k) -> bool {
+            const long long lu = P.last_used[i];
+            if (lu >= f) return false;
+            k = ((unsigned long long)(lu + 1) << slot_bits) | (unsigned long long)i;
+            return true;
+        };
+        const int m = (int)(n < kMaxSel ? n : kMaxSel);
+        int cnt = block_select_smallest(key_of, nf0, m, s, w.lru);
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) w.lru[i] &= (1ll << slot_bits) - 1;
+        n_lru = cnt;
+    }
+    if (threadIdx.x == 0) n_lru_s = n_lru;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long next_free = nf0, lp = 0, loaded = 0, deferred = 0, inserted = 0;
+        for (long long i = 0; i < n; i++) {
+            const long long key = P.staged_keys[i];
+            const int existing = P.table[key];
+            int slot = -1;
+            if (existing >= 0) {
+                slot = existing;
+                P.last_used[slot] = f;
+                w.assign[i] = slot;
+                loaded++;
+                continue;
+            }
+            if (next_free < P.slots) {
+                slot = (int)next_free++;
+            } else {
+                while (lp < n_lru_s && P.last_used[w.lru[lp]] >= f) lp++;
+                if (lp < n_lru_s) slot = (int)w.lru[lp++];
+            }
+            if (slot < 0) {
+                deferred++;
+                w.assign[i] = -1;
+                continue;
+            }
+            const long long old = P.owner[slot];
+            if (old >= 0) P.table[old] = -1;
+            P.owner[slot] = key;
+            P.table[key] = slot;
+            P.last_used[slot] = f;
+            w.assign[i] = slot;
+            inserted++;
+            loaded++;
+        }
+        st->next_free = next_free;
+        st->bricks_loaded = loaded;
+        st->deferred = deferred;
+        st->inserted = inserted;
+        st->loaded_total += inserted;
+    }
+    __syncthreads();
+    const long long b3 = P.geom.b * P.geom.b * P.geom.b;
+    for (long long i = 0; i < n; i++) {
+        const int slot = w.assign[i];
+        if (slot < 0) continue;
+        const float4* src = reinterpret_cast<const float4*>(P.staging + i * b3);
+        float4* dst = reinterpret_cast<float4*>(P.pool + (long long)slot * b3);
+        if ((b3 & 3) == 0) {
+            for (long long t = threadIdx.x; t < b3 / 4; t += blockDim.x) dst[t] = src[t];
+        } else {
+            for (long long t = threadIdx.x; t < b3; t += blockDim.x) P.pool[(long long)slot * b3 + t] = P.staging[i * b3 + t];
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long composite_key(const VcbMaintParams& P, long long b) {
+    const int lod = lod_of(P.geom, b);
+    const unsigned long long lin = (unsigned long long)(b - P.geom.offset[lod]);
+    const int low = P.lin_bits + P.lod_bits;
+    const long long base = P.req_base[b];
+    unsigned long long hi;
+    if (P.ranking) {
+        const long long h = P.req_hits[b];
+        const long long r = (base + h < base + P.rank_clamp) ? base + h : base + P.rank_clamp;
+        const unsigned long long rmax = (1ull << (63 - low)) - 1;
+        hi = rmax - (unsigned long long)r;
+    } else {
+        hi = (unsigned long long)base;
+    }
+    return (hi << low) | (lin << P.lod_bits) | (unsigned long long)lod;
+}
+
+__global__ void k_pending(VcbMaintParams P, MaintWs w) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
+         b += (long long)gridDim.x * blockDim.x) {
+        if (P.req_base[b] < 0) continue;
+        const int o = atomicAdd(&w.ctr[0], 1);
+        w.pend_flat[o] = b;
+        // excluded (is_mapped) entries carry the top bit so a selection over
+        // non-excluded keys can skip them
+        w.pend_key[o] = (long long)composite_key(P, b) | (P.table[b] >= 0 ? (1ll << 63) : 0ll);
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintWs w) {
+    __shared__ SelSmem s;
+    __shared__ long long picked[kMaxSel];
+    VcbCacheState* st = P.state;
+    const long long np = w.ctr[0];
+    const int m = P.max_requests < kMaxSel ? P.max_requests : kMaxSel;
+    auto key_ok = [&](long long i, unsigned long long& k) -> bool {
+        const long long v = w.pend_key[i];
+        if (v < 0) return false;  // excluded (mapped)
+        k = (unsigned long long)v;
+        return true;
+    };
+    const int cnt = block_select_smallest(key_ok, np, m, s, picked);
+    // threshold: the last picked key when n were found, else everything goes
+    const unsigned long long thresh = (cnt >= m && cnt > 0) ? (unsigned long long)picked[cnt - 1] : ~0ull;
+    for (long long i = threadIdx.x; i < np; i += blockDim.x) {
+        const unsigned long long k = (unsigned long long)w.pend_key[i] & ~(1ull << 63);
+        if (k <= thresh) P.req_base[w.pend_flat[i]] = -1;  // popped (returned or dropped)
+    }
+    const unsigned long long lowmask = (1ull << (P.lin_bits + P.lod_bits)) - 1;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const unsigned long long k = (unsigned long long)picked[i] & lowmask;
+        const int lod = (int)(k & ((1ull << P.lod_bits) - 1));
+        const long long lin = (long long)(k >> P.lod_bits);
+        P.staged_keys[i] = P.geom.offset[lod] + lin;
+    }
+    if (threadIdx.x == 0) {
+        st->n_staged = cnt;
+        st->staged_frame = P.session_frame;
+        st->n_inflight = cnt;
+        st->n_pending = np;
+        st->n_batch = cnt;
+        st->n_reports = w.ctr[1];
+    }
+}
+
+__global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* keys, const int64_t* n_keys_dev,
+                                    int max_keys, float* out, int* nonfinite) {
+    extern __shared__ float smem[];
+    MlpSmem m;
+    const long long nk = *n_keys_dev;
+    if (nk == 0) return;
+    const bool fast = F.kind == 0 && inr_is_default(F);
+    if (F.kind == 0) {
+        stage_mlp(F, smem, m);
+        __syncthreads();
+    }
+    const long long b = G.b, b3 = b * b * b;
+    const long long total = nk * b3;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long ki = t / b3, s_ = t - ki * b3;
+        const long long flat = keys[ki];
+        const int lod = lod_of(G, flat);
+        const long long lin = flat - G.offset[lod];
+        const long long gx = G.grid[lod][0], gy = G.grid[lod][1];
+        const long long ix = lin % gx, iy = (lin / gx) % gy, iz = lin / (gx * gy);
+        const long long x = s_ % b, y = (s_ / b) % b, z = s_ / (b * b);
+        long long nx = (ix > 0 ? ix * (b << lod) - 1 : 0) + (x << lod);
+        long long ny = (iy > 0 ? iy * (b << lod) - 1 : 0) + (y << lod);
+        long long nz = (iz > 0 ? iz * (b << lod) - 1 : 0) + (z << lod);
+        nx = nx < G.dims[0] - 1 ? nx : G.dims[0] - 1;
+        ny = ny < G.dims[1] - 1 ? ny : G.dims[1] - 1;
+        nz = nz < G.dims[2] - 1 ? nz : G.dims[2] - 1;
+        int bad = 0;
+        out[t] = field_eval(F, ((double)nx + 0.5) / (double)G.dims[0], ((double)ny + 0.5) / (double)G.dims[1],
+                            ((double)nz + 0.5) / (double)G.dims[2], m, fast, &bad);
+        if (bad) *nonfinite = 1;
+    }
+}
+
+__global__ void k_post_decode(VcbMaintParams P, MaintWs w) {
+    VcbCacheState* st = P.state;
+    if (*w.nonfinite) {
+        // InlineLoader.dispatch failure: keys re-enter with base = f, hits = 0
+        for (long long i = 0; i < st->n_staged; i++) {
+            const long long b = P.staged_keys[i];
+            P.req_base[b] = P.session_frame;
+            P.req_hits[b] = 0;
+        }
+        st->n_staged = 0;
+        st->n_inflight = 0;
+        st->decode_error += 1;
+        *w.nonfinite = 0;
+    }
+}
+
+int mlp_smem_bytes(const VcbField& F);
+
+}  // namespace cinr
+
+using namespace cinr;
+
+extern "C" int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests) {
+    (void)slots;
+    (void)max_requests;
+    return maint_ws_layout(total_bricks, nullptr, nullptr);
+}
+
+extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
+    const VcbMaintParams& P = *pp;
+    cudaStream_t st = (cudaStream_t)stream_;
+    if (P.max_requests < 1) return set_error("maintenance: batch size must be >= 1");
+    if (P.max_requests > kMaxSel) return set_error("maintenance: max_requests > %d unsupported", kMaxSel);
+    MaintWs w;
+    int64_t need = maint_ws_layout(P.total, P.workspace, &w);
+    if (need > P.workspace_bytes) return set_error("maintenance: workspace too small");
+    cudaMemsetAsync(w.ctr, 0, 64, st);
+    const int g = grid_for(P.total, 256, 8);
+    // 1. drain miss reports into the request table (session.py:135-136)
+    k_report<<<g, 256, 0, st>>>(P, w);
+    // 2. collect: insert last dispatch's bricks (session.py:137-140)
+    k_insert<<<1, kSelThreads, 0, st>>>(P, w);
+    // 3. dispatch: select the batch (session.py:141, scheduler.py:152-169)
+    k_pending<<<g, 256, 0, st>>>(P, w);
+    k_select<<<1, kSelThreads, 0, st>>>(P, w);
+    // 4. fulfill into the staging slab (inserted at the next maintenance)
+    const int sm = mlp_smem_bytes(P.field);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_decode_bricks_dev, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
+    k_decode_bricks_dev<<<grid_for((int64_t)P.max_requests * b3, 128, 8), 128, sm, st>>>(
+        P.field, P.geom, P.staged_keys,
+        (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged)), P.max_requests, P.staging,
+        w.nonfinite);
+    k_post_decode<<<1, 1, 0, st>>>(P, w);
+    return check_launch("maintenance");
+}

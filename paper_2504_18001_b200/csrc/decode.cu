@@ -1,0 +1,173 @@
+// Field decoders: brick fill straight into a pool/staging slab, point batches
+// (true misses / Field.sample_batch) and the macro-cell min/max pre-pass.
+//
+// Brick decode (scheduler.py:127-134 fulfill -> brickmath.py:125-139): sample s
+// of a brick is x + B*(y + B*z) (x-fastest == pool [slot,z,y,x], P15); native =
+// clip(origin + (x,y,z)*2^L, 0, V-1), normalized = (native + 0.5)/V in f64.
+#include "common.cuh"
+#include "fields.cuh"
+#include "util.cuh"
+
+namespace cinr {
+
+__device__ __forceinline__ long long brick_origin(long long idx, long long b, int lod) {
+    long long o = idx * (b << lod);
+    return idx > 0 ? o - 1 : o;
+}
+
+__global__ void k_field_bricks(VcbField F, VcbBrickGeom G, int64_t n_keys, const int64_t* __restrict__ keys,
+                               float* __restrict__ out, int32_t* nonfinite) {
+    extern __shared__ float smem[];
+    MlpSmem m;
+    const bool fast = F.kind == 0 && inr_is_default(F);
+    if (F.kind == 0) {
+        stage_mlp(F, smem, m);
+        __syncthreads();
+    }
+    const long long b = G.b, b3 = b * b * b;
+    const long long total = n_keys * b3;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long ki = t / b3, s = t - ki * b3;
+        const long long flat = keys[ki];
+        int lod = 0;
+        while (lod + 1 < G.n_lod && flat >= G.offset[lod + 1]) lod++;
+        const long long lin = flat - G.offset[lod];
+        const long long gx = G.grid[lod][0], gy = G.grid[lod][1];
+        const long long ix = lin % gx, iy = (lin / gx) % gy, iz = lin / (gx * gy);
+        const long long x = s % b, y = (s / b) % b, z = s / (b * b);
+        long long nx = brick_origin(ix, b, lod) + (x << lod);
+        long long ny = brick_origin(iy, b, lod) + (y << lod);
+        long long nz = brick_origin(iz, b, lod) + (z << lod);
+        nx = nx < G.dims[0] - 1 ? nx : G.dims[0] - 1;
+        ny = ny < G.dims[1] - 1 ? ny : G.dims[1] - 1;
+        nz = nz < G.dims[2] - 1 ? nz : G.dims[2] - 1;
+        const double px = ((double)nx + 0.5) / (double)G.dims[0];
+        const double py = ((double)ny + 0.5) / (double)G.dims[1];
+        const double pz = ((double)nz + 0.5) / (double)G.dims[2];
+        int bad = 0;
+        out[t] = field_eval(F, px, py, pz, m, fast, &bad);
+        if (bad) *nonfinite = 1;
+    }
+}
+
+__global__ void k_field_points(VcbField F, int64_t n, const double* __restrict__ pos, float* __restrict__ out,
+                               int32_t* nonfinite) {
+    extern __shared__ float smem[];
+    MlpSmem m;
+    const bool fast = F.kind == 0 && inr_is_default(F);
+    if (F.kind == 0) {
+        stage_mlp(F, smem, m);
+        __syncthreads();
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int bad = 0;
+        out[i] = field_eval(F, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], m, fast, &bad);
+        if (bad) *nonfinite = 1;
+    }
+}
+
+// macrocell.py:49-74: lattice values at voxel centres ((i+0.5)/V), per cell the
+// min/max over the cell dilated by one voxel.  One CTA per cell; the lattice is
+// decoded on the fly (never materialised: 4096^3 would be 275 GB).
+__global__ void k_macro_minmax(VcbField F, long long vx, long long vy, long long vz, long long cell, long long gx,
+                               long long gy, long long gz, float* vmin, float* vmax) {
+    extern __shared__ float smem[];
+    __shared__ float rmin[32], rmax[32];
+    MlpSmem m;
+    const bool fast = F.kind == 0 && inr_is_default(F);
+    if (F.kind == 0) {
+        stage_mlp(F, smem, m);
+        __syncthreads();
+    }
+    for (long long c = blockIdx.x; c < gx * gy * gz; c += gridDim.x) {
+        const long long ci = c % gx, cj = (c / gx) % gy, ck = c / (gx * gy);
+        const long long x0 = ci * cell - 1 > 0 ? ci * cell - 1 : 0, x1 = (ci + 1) * cell + 1 < vx ? (ci + 1) * cell + 1 : vx;
+        const long long y0 = cj * cell - 1 > 0 ? cj * cell - 1 : 0, y1 = (cj + 1) * cell + 1 < vy ? (cj + 1) * cell + 1 : vy;
+        const long long z0 = ck * cell - 1 > 0 ? ck * cell - 1 : 0, z1 = (ck + 1) * cell + 1 < vz ? (ck + 1) * cell + 1 : vz;
+        const long long nx = x1 - x0, ny = y1 - y0, nz = z1 - z0, cnt = nx * ny * nz;
+        float lo = INFINITY, hi = -INFINITY;
+        for (long long t = threadIdx.x; t < cnt; t += blockDim.x) {
+            const long long x = x0 + t % nx, y = y0 + (t / nx) % ny, z = z0 + t / (nx * ny);
+            float v;
+            if (F.kind == 1) {
+                v = __ldg(F.lattice + (z * vy + y) * vx + x);
+            } else {
+                v = field_eval(F, ((double)x + 0.5) / (double)vx, ((double)y + 0.5) / (double)vy,
+                               ((double)z + 0.5) / (double)vz, m, fast, nullptr);
+            }
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            rmin[threadIdx.x >> 5] = lo;
+            rmax[threadIdx.x >> 5] = hi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
+                lo = fminf(lo, rmin[i]);
+                hi = fmaxf(hi, rmax[i]);
+            }
+            vmin[c] = lo;
+            vmax[c] = hi;
+        }
+        __syncthreads();
+    }
+}
+
+int mlp_smem_bytes(const VcbField& F) {
+    if (F.kind != 0) return 0;
+    int nw = 0, nb = 0;
+    for (int L = 0; L < F.n_layers; L++) {
+        nw += F.widths[L] * F.widths[L + 1];
+        nb += F.widths[L + 1];
+    }
+    return (nw + nb) * (int)sizeof(float);
+}
+
+template <typename K>
+static void allow_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace cinr
+
+using namespace cinr;
+
+extern "C" int32_t vcb_field_points(const VcbField* f, int64_t n, const double* pos, float* out, int32_t* nonfinite,
+                                    void* stream) {
+    if (n <= 0) return 0;
+    const int sm = mlp_smem_bytes(*f);
+    allow_smem(k_field_points, sm);
+    k_field_points<<<grid_for(n, 128, 8), 128, sm, (cudaStream_t)stream>>>(*f, n, pos, out, nonfinite);
+    return check_launch("field_points");
+}
+
+extern "C" int32_t vcb_field_bricks(const VcbField* f, const VcbBrickGeom* g, int64_t n_keys, const int64_t* keys,
+                                    float* out, int32_t* nonfinite, void* stream) {
+    if (n_keys <= 0) return 0;
+    const int sm = mlp_smem_bytes(*f);
+    allow_smem(k_field_bricks, sm);
+    const int64_t total = n_keys * g->b * g->b * g->b;
+    k_field_bricks<<<grid_for(total, 128, 8), 128, sm, (cudaStream_t)stream>>>(*f, *g, n_keys, keys, out,
+                                                                                 nonfinite);
+    return check_launch("field_bricks");
+}
+
+extern "C" int32_t vcb_macro_minmax(const VcbField* f, const int64_t* dims, int64_t cell, float* vmin, float* vmax,
+                                    void* stream) {
+    const long long gx = (dims[0] + cell - 1) / cell, gy = (dims[1] + cell - 1) / cell, gz = (dims[2] + cell - 1) / cell;
+    const int sm = mlp_smem_bytes(*f);
+    allow_smem(k_macro_minmax, sm);
+    long long cells = gx * gy * gz;
+    int grid = (int)(cells < (long long)device_sms() * 16 ? cells : (long long)device_sms() * 16);
+    k_macro_minmax<<<grid, 256, sm, (cudaStream_t)stream>>>(*f, dims[0], dims[1], dims[2], cell, gx, gy, gz, vmin,
+                                                            vmax);
+    return check_launch("macro_minmax");
+}

@@ -1,0 +1,265 @@
+"""GPU-resident drop-in for voxcache.session.RenderSession (session.py:26-152).
+
+Same constructor, methods, FrameRecord and frame cycle:
+    render (vcb_march_frame) -> maintenance (vcb_maintenance) -> tick.
+The cache, request table and loader staging live in HBM; the host issues two
+C-ABI calls per frame and reads back one small stats block (plus the image
+when the caller wants it on the host, as the reference API returns it).
+
+Loader semantics are the reference InlineLoader (P12): a batch dispatched at
+maintenance f is decoded into a staging slab on the GPU right away and
+inserted at maintenance f+1.  `loader="thread"` maps to the same deterministic
+schedule (the GPU decode of one batch always completes within a frame).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import macrocell
+from .cache import CacheConfig, DeviceCache
+from .device import device_field, ptr, require_cuda, stream_ptr
+from .errors import ConfigError, ModelCorruptError, RenderError
+from .render import RenderSettings, base_step, camera_rays_setup
+from .sampler import MODES, LodPolicy, effective_lod_scale, force_max_scale, frame_rng_base, point_to_unit_box
+from .scheduler import SchedulerConfig
+
+
+@dataclass
+class SessionConfig:
+    cached: bool = True
+    mode: str = "raymarch"
+    loader: str = "thread"
+    cache: CacheConfig = dc_field(default_factory=CacheConfig)
+    scheduler: SchedulerConfig = dc_field(default_factory=SchedulerConfig)
+    policy: LodPolicy = dc_field(default_factory=LodPolicy)
+    settings: RenderSettings = dc_field(default_factory=RenderSettings)
+    macro_cell_size: int = 16
+    samples_per_pixel: int = 1
+    seed: int = 0
+
+
+@dataclass
+class FrameRecord:
+    frame: int
+    wall_s: float
+    fps: float
+    samples: int
+    true_misses: int
+    fallback_hits: int
+    exact_hits: int
+    occupancy: float
+    bricks_loaded: int
+    bricks_loaded_total: int
+    requests_inflight: int
+
+
+_EPOCH = [1]
+
+
+def _next_epoch() -> int:
+    _EPOCH[0] = (_EPOCH[0] + 1) & 0x3FFFF or 1
+    return _EPOCH[0]
+
+
+class RenderSession:
+    """Owns the device render state for one viewer/bench run."""
+
+    def __init__(self, field_src, tf, camera, config: SessionConfig, macro=None, device=None, debug=False,
+                 stream=None):
+        self.device = require_cuda(device)
+        if config.mode not in ("raymarch",):
+            raise ConfigError("only mode='raymarch' is implemented on the GPU path")
+        if config.loader not in ("inline", "thread"):
+            raise ValueError(f"unknown loader kind {config.loader!r}")
+        self.field = field_src
+        self.config = config
+        self.dims = tuple(int(d) for d in field_src.domain.dims)
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        self._dfield = device_field(field_src, self.device)
+        with torch.cuda.stream(self.stream):
+            self.macro = macro if macro is not None else macrocell.build(field_src, self.dims,
+                                                                          config.macro_cell_size, self.device)
+        self.tf = tf
+        self._set_majorants(tf)
+        self.camera = camera
+        self.debug = debug
+        if config.cached:
+            with torch.cuda.stream(self.stream):
+                self.cache = DeviceCache(self.dims, config.cache, config.scheduler, self.device, debug=debug)
+        else:
+            self.cache = None
+        self.frame = 0
+        self.mode = config.mode
+        self._ws = None
+        self._img = None
+        self._stats = torch.zeros(C.sizeof(N.VcbFrameStats) // 8, dtype=torch.int64, device=self.device)
+        self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
+                                       dtype=torch.int64).pin_memory()
+        self.last_frame_stats = {}
+
+    # -- control (session.py:78-101)
+    def _set_majorants(self, tf):
+        macrocell.update_majorants(self.macro, tf)
+        self._mu = torch.from_numpy(np.ascontiguousarray(self.macro.majorant, dtype=np.float32)).to(self.device)
+        self._lut = torch.from_numpy(np.ascontiguousarray(tf.lookup_table(), dtype=np.float32)).to(self.device)
+
+    def set_camera(self, camera):
+        self.camera = camera
+
+    def set_transfer_function(self, tf):
+        self.tf = tf
+        self._set_majorants(tf)
+
+    def set_lod_scale(self, scale: float):
+        self.config.policy.lod_scale = float(scale)
+
+    def set_mode(self, mode: str):
+        if mode not in ("raymarch", "pathtrace"):
+            raise ValueError(f"unknown mode {mode!r}")
+        if mode != "raymarch":
+            raise ConfigError("pathtrace is out of scope for the GPU path")
+        self.mode = mode
+
+    def reset_cache(self):
+        if self.cache is not None:
+            with torch.cuda.stream(self.stream):
+                self.cache.reset()
+        self.frame = 0
+
+    # -- frame cycle (session.py:105-130)
+    def _frame_params(self, image):
+        cam = self.camera
+        cfg = self.config
+        s = cfg.settings
+        W, H = int(cam.width), int(cam.height)
+        p = N.VcbFrameParams()
+        rot, tan_h, tan_v = camera_rays_setup(cam)
+        for a in range(3):
+            p.cam.origin[a] = float(cam.position[a])
+        for i in range(9):
+            p.cam.rot[i] = float(rot.ravel()[i])
+        p.cam.tan_h, p.cam.tan_v, p.cam.width, p.cam.height = tan_h, tan_v, W, H
+        vx, vy, vz = self.dims
+        m = self.macro
+        p.adv.adaptive = 1 if s.adaptive_step else 0
+        p.adv.skip_empty = 1 if s.skip_empty else 0
+        p.adv.dt_base = base_step(self.dims, s)
+        p.adv.mu_floor = float(s.mu_floor)
+        p.adv.gx, p.adv.gy, p.adv.gz = m.grid_dims
+        p.adv.cwx, p.adv.cwy, p.adv.cwz = m.cell_size / vx, m.cell_size / vy, m.cell_size / vz
+        pol = cfg.policy
+        if pol.mode not in MODES:
+            raise ValueError(f"unknown stochastic lod mode {pol.mode!r}")
+        c = self.cache
+        if c is not None:
+            force = force_max_scale(c.max_lod, point_to_unit_box(np.asarray(cam.position, dtype=np.float64)))
+            scale = effective_lod_scale(pol, self.frame, force)
+            lay = c.layout
+            p.probe.vx, p.probe.vy, p.probe.vz = float(vx), float(vy), float(vz)
+            p.probe.lod_scale = scale
+            p.probe.mode = MODES[pol.mode]
+            p.probe.max_lod = c.max_lod
+            p.probe.b = lay.brick_size
+            p.probe.b_pow2 = 1 if (lay.brick_size & (lay.brick_size - 1)) == 0 else 0
+            for l in range(c.max_lod + 1):
+                for a in range(3):
+                    p.probe.grid[l][a] = lay.grids[l][a]
+                p.probe.offset[l] = lay.offsets[l]
+            p.cached = 1
+            p.paged_dist = 1 if c.paged else 0
+            p.cache_frame = c.frame
+            p.table, p.pool, p.last_used, p.miss_count = ptr(c.table), ptr(c.pool), ptr(c.last_used), ptr(c.miss_count)
+        p.rng_base = frame_rng_base(cfg.seed, self.frame)
+        p.term = float(s.early_termination)
+        for a in range(3):
+            p.bg[a] = float(s.background[a])
+        p.lut_size = self._lut.shape[0]
+        p.max_iterations = int(s.max_iterations)
+        p.epoch = _next_epoch()
+        p.mu, p.lut = ptr(self._mu), ptr(self._lut)
+        p.field = self._dfield.desc
+        p.image = ptr(image)
+        p.stats = ptr(self._stats)
+        need = N.load().vcb_frame_workspace_bytes(W * H, p.max_iterations)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        p.workspace = ptr(self._ws)
+        p.workspace_bytes = self._ws.numel()
+        return p
+
+    def render_frame_device(self):
+        """Render + maintenance on the session stream; returns the device image
+        (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame."""
+        W, H = int(self.camera.width), int(self.camera.height)
+        if self._img is None or self._img.shape != (H, W, 4):
+            self._img = torch.empty((H, W, 4), dtype=torch.float32, device=self.device)
+        img = self._img
+        with torch.cuda.stream(self.stream):
+            self._stats.zero_()
+            p = self._frame_params(img)
+            N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
+            if self.cache is not None:
+                self.cache.maintenance(self.frame, self._dfield.desc, self.stream)
+            # one small D2H for the FrameRecord counters
+            ns = self._stats.numel()
+            self._host_stats[:ns].copy_(self._stats, non_blocking=True)
+            if self.cache is not None:
+                self._host_stats[ns:].copy_(self.cache.state, non_blocking=True)
+        return img
+
+    def collect_record(self, t0: float) -> FrameRecord:
+        self.stream.synchronize()
+        hs = self._host_stats.numpy()
+        ns = self._stats.numel()
+        fs = {f[0]: int(hs[i]) for i, f in enumerate(N.VcbFrameStats._fields_) if f[0] != "pad_"}
+        self.last_frame_stats = fs
+        if fs["nonfinite"]:
+            raise RenderError("miss resolution failed: inference produced non-finite outputs")
+        wall = time.perf_counter() - t0
+        c = self.cache
+        if c is not None:
+            st = {f[0]: int(hs[ns + i]) for i, f in enumerate(N.VcbCacheState._fields_) if f[0] != "pad_"}
+            self.last_cache_state = st
+            rec = FrameRecord(self.frame, wall, 1.0 / wall if wall > 0 else float("inf"), fs["requests"], fs["miss"],
+                              fs["fallback"], fs["exact"], 1.0 - (c.slots - st["next_free"]) / c.slots,
+                              st["bricks_loaded"], st["loaded_total"], st["n_inflight"])
+            c.frame += 1
+        else:
+            rec = FrameRecord(self.frame, wall, 1.0 / wall if wall > 0 else float("inf"), fs["requests"], fs["miss"],
+                              0, 0, 0.0, 0, 0, 0)
+        self.frame += 1
+        return rec
+
+    def render_frame(self):
+        """Render, then run the maintenance phase; returns (image f32[H,W,4] on host, FrameRecord)."""
+        t0 = time.perf_counter()
+        img = self.render_frame_device()
+        host = torch.empty(img.shape, dtype=torch.float32, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            host.copy_(img, non_blocking=True)
+        rec = self.collect_record(t0)
+        return host.numpy(), rec
+
+    def debug_state(self):
+        """Reference-shaped per-frame state (tables, owner, stamps, requests, batch, reports)."""
+        self.stream.synchronize()
+        d = self.cache.dump()
+        d["batch"] = self.cache.batch()
+        d["reports"] = self.cache.reports()
+        return d
+
+    def close(self):
+        self.stream.synchronize()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
