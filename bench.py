@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Headline benchmark: cached-INR ray-march frames/s at 1024^2 (BASELINE.json config 2).
+
+Workload (configs[1]): 512^3 volume decoded from the random-init hash-grid INR
+(HashGridConfig()/MLPConfig(), seed 0, parameters re-drawn uniform(-0.7,0.7) from
+default_rng(42)), 16^3 bricks, 32^3-slot pool (537 MB), 1024x1024 frames on the
+orbit (center .5, radius 2.2, 120 frames/rev, 20 deg elevation, fov 45),
+warm_body(0.5, 0.9), LodPolicy(1.2, preload 20), 40 requests/frame, inline
+loader (deterministic), seed 0.  A step = one RenderSession.render_frame()
+(render + maintenance), the reference's fps definition (session.py:107-113).
+
+  value : frames/s with everything resident in HBM (device-side render + stats
+          readback), CUDA events on the session stream, L2 flushed between frames
+  e2e   : the same frames through the public API render_frame() returning the
+          host image (D2H inside the timed region)
+  cpu_baseline : the CPU oracle (restated reference, all host threads) rendering
+          the same steady-state frame from the GPU session's exact cache state
+
+Multi-GPU (torchrun, N>1): sort-first horizontal bands, one private cache per GPU,
+band images all-gathered with NCCL every frame (scaling "strong": one full frame
+per step, split over N GPUs).
+
+`--impl reference` times the CPU oracle port alone (the reference path has no GPU
+code) on a bounded sample of the same workload; see the JSON `cpu_baseline.sample`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec at 1024^2 (cached INR render, 512^3 random-init INR, config 2)"
+UNIT = "frames/s"
+BYTES_PER_SAMPLE = 40  # 8 f32 corners + 1 i32 page-table entry + 1 f32 majorant
+
+
+def workload(res=1024, volume=512, pool=32):
+    return dict(workload="config2_cached_inr_raymarch", volume=f"{volume}^3 random-init INR (8x2 hash grid, 16-32-32-1)",
+                image=f"{res}x{res}", brick=16, pool_slots=pool ** 3, orbit="r=2.2, 120 frames/rev, elev 20, fov 45",
+                tf="warm_body(0.5,0.9)", lod_policy="scale 1.2, preload 20, corrected", max_requests=40,
+                loader="inline", l2="flushed (256 MB write) between timed frames")
+
+
+def make_model(volume):
+    import paper_2504_18001_b200 as P
+
+    m = P.InrModel(P.HashGridConfig(), P.MLPConfig(), P.FieldDomain((volume,) * 3), seed=0)
+    r = np.random.default_rng(42)
+    m.set_parameters([r.uniform(-0.7, 0.7, size=p.shape).astype(np.float32) for p in m.parameters()])
+    return m
+
+
+def load_macro(volume):
+    f = ROOT / "bench_data" / f"macro_inr{volume}_c16.npz"
+    if f.exists():
+        d = np.load(f)
+        return d["vmin"], d["vmax"], "bench_data (CPU-oracle-built, shared by every arm)"
+    return None, None, "built on the GPU (vcb_macro_minmax)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    f = ROOT / "profiles" / "ncu_march_iter.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# --------------------------------------------------------------------------- CPU arms
+def cpu_oracle_frame_from_state(state, macro, res_frac, frame_idx, volume):
+    """One steady-state frame of the oracle from the GPU session's exact state."""
+    from oracle import cinr_oracle as O
+
+    t, w, b = O.inr_params_from_seed(O.DEFAULT_GRID, O.DEFAULT_MLP)
+    fld = O.InrFieldOracle((volume,) * 3, t, w, b, O.DEFAULT_GRID)
+    cfg = O.Config(dims=(volume,) * 3, brick=16, pool=(32, 32, 32), max_requests=40, lod_scale=1.2, preload=20)
+    sess = O.OracleSession(fld, O.warm_body_points(0.5, 0.9), cfg, macro_minmax_arrays=macro)
+    O.load_session_state(sess, state)
+    res = int(1024 * res_frac)
+    pos = O.orbit_camera((0.5, 0.5, 0.5), 2.2, 120, frame_idx)
+    sess.set_camera(pos, (0.5, 0.5, 0.5), (0.0, 1.0, 0.0), 45.0, res, res)
+    t0 = time.perf_counter()
+    img, rec = sess.render_frame()
+    return time.perf_counter() - t0, img, rec
+
+
+def run_reference_arm(args):
+    """`--impl reference`: the CPU oracle port (the reference has no GPU path) on all
+    host threads; each step = one frame of the config-2 orbit at a reduced image size,
+    fps scaled to 1024^2 by the pixel ratio."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cinr_oracle as O
+
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    vmin, vmax, msrc = load_macro(args.volume)
+    t, w, b = O.inr_params_from_seed(O.DEFAULT_GRID, O.DEFAULT_MLP)
+    fld = O.InrFieldOracle((args.volume,) * 3, t, w, b, O.DEFAULT_GRID)
+    if vmin is None:
+        vmin, vmax = O.macro_minmax_streamed(fld, (args.volume,) * 3, 16)
+    cfg = O.Config(dims=(args.volume,) * 3, brick=16, pool=(32, 32, 32), max_requests=40, lod_scale=1.2, preload=20)
+    sess = O.OracleSession(fld, O.warm_body_points(0.5, 0.9), cfg, macro_minmax_arrays=(vmin, vmax))
+    res = args.ref_res
+    walls = []
+    for f in range(args.warmup + args.steps):
+        pos = O.orbit_camera((0.5, 0.5, 0.5), 2.2, 120, f)
+        sess.set_camera(pos, (0.5, 0.5, 0.5), (0.0, 1.0, 0.0), 45.0, res, res)
+        img, rec = sess.render_frame()
+        if f >= args.warmup:
+            walls.append(rec.wall_s)
+    scale = (res * res) / (args.res * args.res)
+    fps = len(walls) / sum(walls) * scale if walls else 0.0
+    sample = (f"oracle port (C+numpy restatement of voxcache, OpenMP {cores} threads), orbit frames "
+              f"{args.warmup}..{args.warmup + args.steps - 1} rendered at {res}^2 from a cold cache after "
+              f"{args.warmup} warm-up frames; fps scaled x{scale:.4f} (pixel ratio) to {args.res}^2")
+    line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / fps if fps else None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": workload(args.res, args.volume), "impl": "reference",
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--res", type=int, default=1024)
+    ap.add_argument("--volume", type=int, default=512)
+    ap.add_argument("--ref-res", type=int, default=128)
+    ap.add_argument("--cpu-frac", type=float, default=0.25, help="oracle baseline image fraction of --res")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+
+    from paper_2504_18001_b200 import parallel
+    from paper_2504_18001_b200.harness import OrbitTrajectory
+    from paper_2504_18001_b200.macrocell import MacroCellGrid, layout
+    from paper_2504_18001_b200.session import SessionConfig
+
+    import paper_2504_18001_b200 as P
+
+    ctx = parallel.init_from_env()
+    dev = torch.device("cuda", ctx.local_rank)
+    torch.cuda.set_device(dev)
+    model = make_model(args.volume)
+    fld = model.as_field()
+    vmin, vmax, msrc = load_macro(args.volume)
+    t_macro = None
+    if vmin is None:
+        from paper_2504_18001_b200 import macrocell
+
+        t0 = time.perf_counter()
+        mg = macrocell.build(fld, (args.volume,) * 3, 16, dev)
+        t_macro = time.perf_counter() - t0
+    else:
+        grid, _, _ = layout((args.volume,) * 3, 16)
+        mg = MacroCellGrid(16, (args.volume,) * 3, grid, vmin, vmax, np.ones_like(vmin))
+    cfg = SessionConfig(cached=True, loader="inline", cache=P.CacheConfig(brick_size=16, pool_dims=(32, 32, 32)),
+                        scheduler=P.SchedulerConfig(max_requests=40), policy=P.LodPolicy(1.2, 20),
+                        settings=P.RenderSettings(), seed=0)
+    traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=args.res, height=args.res)
+    sess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    st = sess.stream
+
+    def frame_device(f):
+        sess.set_camera(traj.camera_at(f))
+        t0 = time.perf_counter()
+        img = sess.render_frame_device()
+        return img, t0
+
+    # warm-up (cold cache fills; untimed)
+    for f in range(args.warmup):
+        img, t0 = frame_device(f)
+        sess.collect_record(t0)
+        parallel.gather_frame(ctx, img, st)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident frames, one CUDA event pair per frame on the session stream
+    sess.timing = True
+    times, samples, march_ms, march_launches, launches, recs = [], 0, 0.0, 0, 0, []
+    from paper_2504_18001_b200 import _native as N
+
+    with ClockSampler(ctx.local_rank) as clk:
+        for i in range(args.steps):
+            f = args.warmup + i
+            flush.zero_()
+            torch.cuda.synchronize()
+            parallel.barrier(ctx)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            img, t0 = frame_device(f)
+            parallel.gather_frame(ctx, img, st)
+            e1.record(st)
+            rec = sess.collect_record(t0)
+            launches += N.load().vcb_last_launch_count()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            times.append(parallel.max_over_ranks(ctx, ms))
+            samples += rec.samples
+            recs.append(rec)
+            km, kn = sess.march_kernel_time()
+            march_ms += km
+            march_launches += kn
+    sess.timing = False
+    total_ms = sum(times)
+    fps = args.steps / (total_ms / 1000.0)
+    samples_all = parallel.sum_over_ranks(ctx, samples)
+
+    # ---- e2e through the public API (host image out), continuing the orbit
+    e2e = None
+    if not args.no_e2e:
+        walls = []
+        for i in range(args.steps):
+            f = args.warmup + args.steps + i
+            flush.zero_()
+            torch.cuda.synchronize()
+            parallel.barrier(ctx)
+            sess.set_camera(traj.camera_at(f))
+            t0 = time.perf_counter()
+            if ctx.world == 1:
+                img_h, rec = sess.render_frame()
+            else:
+                img = sess.render_frame_device()
+                full = parallel.gather_frame(ctx, img, st)
+                img_h = full.cpu().numpy() if ctx.rank == 0 else None
+                rec = sess.collect_record(t0)
+            walls.append(parallel.max_over_ranks(ctx, (time.perf_counter() - t0) * 1000.0))
+        h2d = len(bytes(N.VcbFrameParams())) + len(bytes(N.VcbMaintParams()))
+        e2e = {"value": args.steps / (sum(walls) / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": args.res * args.res * 16 + 256,
+               "note": "RenderSession.render_frame(): camera/params by value, image f32[H,W,4] copied to host"}
+
+    # ---- CPU baseline (rank 0, N=1): the oracle renders the first timed frame's successor
+    cpu = None
+    if ctx.world == 1 and not args.no_cpu_baseline:
+        try:
+            state = sess.export_state()
+            frac = args.cpu_frac
+            wall, oimg, orec = cpu_oracle_frame_from_state(state, (mg.value_min, mg.value_max), frac, sess.frame,
+                                                            args.volume)
+            cores = os.cpu_count() or 1
+            cpu = {"value": (frac * frac) / wall, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": (f"1 steady-state frame (orbit frame {sess.frame}) rendered by the oracle port "
+                              f"(C+numpy restatement of voxcache, OpenMP {cores} threads) from the GPU session's exact "
+                              f"cache/request/loader state at {int(args.res * frac)}^2, render+maintenance "
+                              f"{wall:.2f}s, fps scaled by the pixel ratio {frac * frac:.4f}")}
+        except Exception as exc:  # the baseline is reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+
+    peak, peak_src = measured_peak_hbm()
+    achieved = (samples_all * BYTES_PER_SAMPLE) / (march_ms / 1000.0) / 1e9 if march_ms > 0 else None
+    if ctx.rank == 0:
+        last = recs[-1]
+        line = {
+            "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 addressing + f32 samples",
+            "data": "synthetic (random-init INR weights, procedural orbit)",
+            "config": {**workload(args.res, args.volume), "parallelism": f"sort-first bands x{ctx.world}",
+                       "macro": msrc},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(),
+                         "kernel": "k_march_iter (advance+rank+probe+shade, per wavefront iteration)",
+                         "algorithmic_bytes": f"{BYTES_PER_SAMPLE} B/sample x samples per launch",
+                         "launches": march_launches, "avg_launch_us": 1000.0 * march_ms / max(march_launches, 1),
+                         "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+            "samples_per_frame": samples_all / args.steps,
+            "inr_samples_per_frame": float(np.mean([r.true_misses for r in recs])) + 40 * 16 ** 3,
+            "hit_rate": 1.0 - sum(r.true_misses for r in recs) / max(1, sum(r.samples for r in recs)),
+            "last_record": {k: getattr(last, k) for k in ("frame", "samples", "true_misses", "fallback_hits",
+                                                          "exact_hits", "occupancy", "bricks_loaded_total")},
+        }
+        if t_macro is not None:
+            line["macro_build_s"] = t_macro
+        print(json.dumps(line), flush=True)
+    parallel.shutdown(ctx)
+
+
+if __name__ == "__main__":
+    main()

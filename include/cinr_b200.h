@@ -45,12 +45,16 @@ extern "C" {
 #define VCB_MAX_LAYERS 8
 
 /* camera.py:129-138: origin, rot = [right, up, fwd] as columns (row-major 3x3),
- * tan_h = tan(fov/2)*aspect, tan_v = tan(fov/2). */
+ * tan_h = tan(fov/2)*aspect, tan_v = tan(fov/2).  A session may render a
+ * subset of the film rows (sort-first multi-GPU): local row j is film row
+ * row0 + j*row_step, `rows` rows in total (row0=0, row_step=1, rows=height
+ * for the whole frame). */
 typedef struct {
     double origin[3];
     double rot[9];
     double tan_h, tan_v;
     int32_t width, height;
+    int32_t row0, row_step, rows, pad_;
 } VcbCamera;
 
 /* advance_pass scalars (kernels.py:35-39). gx/gy/gz macro grid, cw* cell widths. */
@@ -140,7 +144,7 @@ typedef struct {
     int32_t lut_size;
     int32_t max_iterations;
     uint32_t epoch;          /* monotonic per call; tags look-back status words */
-    int32_t pad_;
+    int32_t timing;          /* 1 = bracket every iteration kernel with CUDA events */
     const float *mu;         /* majorants [gz][gy][gx] */
     const float *lut;        /* [lut_size][4] */
     const int32_t *table;    /* dense logical MRPD, all LoDs */
@@ -200,6 +204,9 @@ int32_t vcb_shade_pass(int64_t n, const int64_t *rows, const float *values, cons
                        int64_t lut_size, int32_t adaptive, double dt_base, double term, double *color, double *trans,
                        uint8_t *dead, void *stream);
 
+/* diagnostics: the shade's accurate pow, out[i] = x[i]**y[i] (x in (0,1], y > 0) */
+int32_t vcb_debug_pow(int64_t n, const double *x, const double *y, double *out, void *stream);
+
 /* ---- field / decoder ABI */
 int32_t vcb_field_points(const VcbField *f, int64_t n, const double *pos, float *out, int32_t *nonfinite,
                          void *stream);
@@ -211,6 +218,11 @@ int32_t vcb_macro_minmax(const VcbField *f, const int64_t *dims, int64_t cell, f
 /* ---- session ABI */
 int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);
 int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);
+/* After the stream of a timing=1 frame has completed: summed device time (ms) and
+ * count of the first `n_iters` iteration-kernel launches (the ray-march kernel). */
+int32_t vcb_march_timing(int32_t n_iters, double *ms_total, int64_t *launches);
+/* Kernels launched by this thread's last march_frame + maintenance calls. */
+int64_t vcb_last_launch_count(void);
 int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests);
 int32_t vcb_maintenance(const VcbMaintParams *p, void *stream);
 

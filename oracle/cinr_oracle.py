@@ -763,3 +763,49 @@ class OracleSession:
             c.tick()
         self.frame += 1
         return img, rec
+
+
+def macro_minmax_streamed(fld, dims, cell, slab=None):
+    """macrocell.py:49-74 without materialising the lattice: evaluate the field one
+    slab of cell z-layers (+1 halo each side) at a time."""
+    vx, vy, vz = dims
+    g = [-(-v // cell) for v in (vx, vy, vz)]
+    vmin = np.empty((g[2], g[1], g[0]), dtype=np.float32)
+    vmax = np.empty_like(vmin)
+    ys, xs = np.meshgrid((np.arange(vy) + 0.5) / vy, (np.arange(vx) + 0.5) / vx, indexing="ij")
+    for k in range(g[2]):
+        z0, z1 = max(k * cell - 1, 0), min((k + 1) * cell + 1, vz)
+        zs = (np.arange(z0, z1) + 0.5) / vz
+        pos = np.empty((z1 - z0, vy, vx, 3))
+        pos[..., 0] = xs[None]
+        pos[..., 1] = ys[None]
+        pos[..., 2] = zs[:, None, None]
+        lat = fld.sample(pos.reshape(-1, 3)).reshape(z1 - z0, vy, vx)
+        for j in range(g[1]):
+            y0, y1 = max(j * cell - 1, 0), min((j + 1) * cell + 1, vy)
+            for i in range(g[0]):
+                x0, x1 = max(i * cell - 1, 0), min((i + 1) * cell + 1, vx)
+                blk = lat[:, y0:y1, x0:x1]
+                vmin[k, j, i] = blk.min()
+                vmax[k, j, i] = blk.max()
+    return vmin, vmax
+
+
+def load_session_state(sess: "OracleSession", st: dict):
+    """Adopt a cache/request/loader state captured from another implementation
+    (bench.py's CPU baseline starts from the GPU session's exact state, so both
+    render the same steady-state frame)."""
+    c = sess.cache
+    c.table[:] = st["tables"]
+    c.pool[:] = st["pool"]
+    c.owner[:] = st["owner"]
+    c.last_used[:] = st["last_used"]
+    nf = int(st["next_free"])
+    c.free = list(range(c.slots - 1, nf - 1, -1))
+    c.frame = int(st["cache_frame"])
+    c.loaded_total = int(st["loaded_total"])
+    sess.req.entries = {(int(e[0]), int(e[1])): [int(e[2]), int(e[3])] for e in st["entries"]}
+    sess.staged = [((int(k[0]), int(k[1])), np.asarray(v, dtype=np.float32)) for k, v in zip(st["staged_keys"],
+                                                                                         st["staged_data"])]
+    sess.in_flight = set(k for k, _ in sess.staged)
+    sess.frame = int(st["session_frame"])

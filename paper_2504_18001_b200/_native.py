@@ -34,7 +34,8 @@ vp = C.c_void_p
 
 
 class VcbCamera(C.Structure):
-    _fields_ = [("origin", f64 * 3), ("rot", f64 * 9), ("tan_h", f64), ("tan_v", f64), ("width", i32), ("height", i32)]
+    _fields_ = [("origin", f64 * 3), ("rot", f64 * 9), ("tan_h", f64), ("tan_v", f64), ("width", i32), ("height", i32),
+                ("row0", i32), ("row_step", i32), ("rows", i32), ("pad_", i32)]
 
 
 class VcbMarchStatic(C.Structure):
@@ -75,7 +76,7 @@ class VcbCacheState(C.Structure):
 class VcbFrameParams(C.Structure):
     _fields_ = [("cam", VcbCamera), ("adv", VcbMarchStatic), ("probe", VcbProbeStatic), ("cached", i32),
                 ("paged_dist", i32), ("cache_frame", i64), ("rng_base", C.c_uint64), ("term", f64), ("bg", f64 * 3),
-                ("lut_size", i32), ("max_iterations", i32), ("epoch", C.c_uint32), ("pad_", i32),
+                ("lut_size", i32), ("max_iterations", i32), ("epoch", C.c_uint32), ("timing", i32),
                 ("mu", vp), ("lut", vp), ("table", vp), ("pool", vp), ("last_used", vp), ("miss_count", vp),
                 ("field", VcbField), ("image", vp), ("stats", vp), ("workspace", vp), ("workspace_bytes", i64),
                 ("reserved_", i64)]
@@ -98,11 +99,14 @@ _PROTOS = {
     "vcb_advance_pass": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, C.POINTER(VcbMarchStatic), vp, vp, vp, vp, vp, vp, vp]),
     "vcb_probe_pass": (i32, [i64, vp, vp, vp, C.POINTER(VcbProbeStatic), vp, vp, vp, i64, vp, vp, vp, vp, vp]),
     "vcb_shade_pass": (i32, [i64, vp, vp, vp, vp, i64, i32, f64, f64, vp, vp, vp, vp]),
+    "vcb_debug_pow": (i32, [i64, vp, vp, vp, vp]),
     "vcb_field_points": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),
     "vcb_field_bricks": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
     "vcb_macro_minmax": (i32, [C.POINTER(VcbField), vp, i64, vp, vp, vp]),
     "vcb_frame_workspace_bytes": (i64, [i64, i32]),
     "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),
+    "vcb_march_timing": (i32, [i32, vp, vp]),
+    "vcb_last_launch_count": (i64, []),
     "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
     "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
 }

@@ -376,6 +376,7 @@ __global__ void k_post_decode(VcbMaintParams P, MaintWs w) {
 }
 
 int mlp_smem_bytes(const VcbField& F);
+extern thread_local long long g_launches;
 
 }  // namespace cinr
 
@@ -413,5 +414,6 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
         (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged)), P.max_requests, P.staging,
         w.nonfinite);
     k_post_decode<<<1, 1, 0, st>>>(P, w);
+    g_launches += 6;
     return check_launch("maintenance");
 }

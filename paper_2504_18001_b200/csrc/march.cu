@@ -14,6 +14,7 @@
 // preserved by every compaction, so the rank of a ray among the rays sampling
 // in iteration k equals the lane index numpy's flatnonzero() gives it (P5/P18).
 #include <cstdio>
+#include <vector>
 
 #include "common.cuh"
 #include "fields.cuh"
@@ -113,6 +114,11 @@ __global__ void k_shade_pass(int64_t n, const int64_t* __restrict__ rows, const 
     }
 }
 
+__global__ void k_pow_dd(int64_t n, const double* x, const double* y, double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = pow_dd(x[i], y[i]);
+}
+
 // ----------------------------------------------------------------- frame march
 __device__ __forceinline__ void retire(const VcbFrameParams& p, int pix, double cr, double cg, double cb, double tr) {
     // raymarch.py:57-60: rgb = color + T*bg, alpha = 1 - T, then .astype(float32)
@@ -127,11 +133,11 @@ __device__ __forceinline__ void retire(const VcbFrameParams& p, int pix, double 
 // Pixel pass: background everywhere (raymarch.py:33-35), box hits flagged.
 __global__ void k_raygen_frame(VcbFrameParams p, FrameWs w) {
     const int W = p.cam.width, H = p.cam.height;
-    const int64_t n = (int64_t)W * H;
+    const int64_t n = (int64_t)W * p.cam.rows;
     float4 bg = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double fx, fy;
-        film_coord((int)(i % W), (int)(i / W), W, H, fx, fy);
+        film_coord((int)(i % W), p.cam.row0 + (int)(i / W) * p.cam.row_step, W, H, fx, fy);
         Ray r = make_ray(fx, fy, p.cam);
         reinterpret_cast<float4*>(p.image)[i] = bg;
         w.pix_keep[i] = r.keep ? 1 : 0;
@@ -143,7 +149,7 @@ __global__ void k_raygen_frame(VcbFrameParams p, FrameWs w) {
 __global__ void __launch_bounds__(kTile) k_compact_rays(VcbFrameParams p, FrameWs w) {
     __shared__ ScanSmem sm;
     const int W = p.cam.width, H = p.cam.height;
-    const int64_t n = (int64_t)W * H;
+    const int64_t n = (int64_t)W * p.cam.rows;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     for (;;) {
         if (threadIdx.x == 0) sm.tile = atomicAdd(&w.ctr->ticket_rays, 1);
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(kTile) k_compact_rays(VcbFrameParams p, FrameW
         uint32_t total = ordered_scan(flag, tile, w.status, p.epoch * 16384u + 16383u, sm, excl);
         if (flag) {
             double fx, fy;
-            film_coord((int)(i % W), (int)(i / W), W, H, fx, fy);
+            film_coord((int)(i % W), p.cam.row0 + (int)(i / W) * p.cam.row_step, W, H, fx, fy);
             Ray r = make_ray(fx, fy, p.cam);
             const int64_t j = excl;
             w.ray_pix[j] = (int32_t)i;
@@ -380,6 +386,12 @@ extern "C" int32_t vcb_raygen_pass(int64_t n, const double* base, const double* 
     return check_launch("raygen_pass");
 }
 
+extern "C" int32_t vcb_debug_pow(int64_t n, const double* x, const double* y, double* out, void* stream) {
+    if (n <= 0) return 0;
+    k_pow_dd<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, y, out);
+    return check_launch("debug_pow");
+}
+
 extern "C" int32_t vcb_advance_pass(int64_t n, const double* o, const double* d, const double* t_en,
                                     const double* t_ex, double* cursor_f, int64_t* cursor_k, const uint8_t* active,
                                     const VcbMarchStatic* s, const float* mu, double* out_pos, double* out_dt,
@@ -410,6 +422,12 @@ extern "C" int32_t vcb_shade_pass(int64_t n, const int64_t* rows, const float* v
     return check_launch("shade_pass");
 }
 
+namespace cinr {
+thread_local long long g_launches = 0;
+static thread_local std::vector<cudaEvent_t> g_ev;
+static thread_local int g_ev_used = 0;
+}  // namespace cinr
+
 static unsigned long long* mapped_live(int n, unsigned long long** dev) {
     // pinned + mapped host array the iteration kernels write live counts into,
     // so the host loop can stop issuing iterations without a stream sync
@@ -434,7 +452,7 @@ static unsigned long long* mapped_live(int n, unsigned long long** dev) {
 extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     const VcbFrameParams& p = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
-    const int64_t npix = (int64_t)p.cam.width * p.cam.height;
+    const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
     FrameWs w;
     int64_t need = frame_ws_layout(npix, max_it, p.workspace, &w);
@@ -465,6 +483,15 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     // host waits for chunk c-1 and stops once its last live count (tagged with this
     // frame's epoch) is zero.  Iterations past the end exit on live[k] == 0.
     const int chunk = 16;
+    g_launches = 2;
+    if (p.timing) {
+        while ((int)g_ev.size() < 2 * max_it) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            g_ev.push_back(e);
+        }
+    }
+    g_ev_used = 0;
     cudaEvent_t ev[2];
     cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
@@ -474,9 +501,13 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     while (k < max_it && !stop) {
         const int kend = k + chunk < max_it ? k + chunk : max_it;
         for (; k < kend; k++) {
+            if (p.timing) cudaEventRecord(g_ev[2 * k], st);
             k_march_iter<<<iter_grid, kTile, 0, st>>>(p, w, k, dlive);
+            if (p.timing) cudaEventRecord(g_ev[2 * k + 1], st);
             k_miss_shade<<<sms * 4, 256, smem_mlp, st>>>(p, w, k);
+            g_launches += 2;
         }
+        if (p.timing) g_ev_used = k;
         cudaEventRecord(ev[ci & 1], st);
         chunk_end[ci & 1] = kend;
         ci++;
@@ -489,7 +520,24 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     }
     k_flush<<<grid_for(npix, 256), 256, 0, st>>>(p, w, k);
     k_frame_stats<<<1, 1, 0, st>>>(p, w, k);
+    g_launches += 2;
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
     return check_launch("march_frame");
 }
+
+extern "C" int32_t vcb_march_timing(int32_t n_iters, double* ms_total, int64_t* launches) {
+    double tot = 0.0;
+    int n = n_iters < g_ev_used ? n_iters : g_ev_used;
+    for (int k = 0; k < n; k++) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g_ev[2 * k], g_ev[2 * k + 1]) != cudaSuccess)
+            return set_error("march_timing: %s", cudaGetErrorString(cudaGetLastError()));
+        tot += ms;
+    }
+    *ms_total = tot;
+    *launches = n;
+    return 0;
+}
+
+extern "C" int64_t vcb_last_launch_count(void) { return g_launches; }

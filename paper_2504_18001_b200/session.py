@@ -103,6 +103,18 @@ class RenderSession:
         self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
+        self.timing = False
+        self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
+
+    def set_band(self, row0: int, row_step: int):
+        """Render only film rows row0 + j*row_step (one rank's share of a frame)."""
+        if row_step < 1 or not 0 <= row0 < row_step:
+            raise ValueError("band needs 0 <= row0 < row_step")
+        self.band = (int(row0), int(row_step))
+
+    def _band_rows(self, H: int) -> int:
+        row0, step = self.band
+        return max(0, (H - row0 + step - 1) // step)
 
     # -- control (session.py:78-101)
     def _set_majorants(self, tf):
@@ -146,6 +158,8 @@ class RenderSession:
         for i in range(9):
             p.cam.rot[i] = float(rot.ravel()[i])
         p.cam.tan_h, p.cam.tan_v, p.cam.width, p.cam.height = tan_h, tan_v, W, H
+        row0, step = self.band
+        p.cam.row0, p.cam.row_step, p.cam.rows = row0, step, self._band_rows(H)
         vx, vy, vz = self.dims
         m = self.macro
         p.adv.adaptive = 1 if s.adaptive_step else 0
@@ -183,11 +197,12 @@ class RenderSession:
         p.lut_size = self._lut.shape[0]
         p.max_iterations = int(s.max_iterations)
         p.epoch = _next_epoch()
+        p.timing = 1 if self.timing else 0
         p.mu, p.lut = ptr(self._mu), ptr(self._lut)
         p.field = self._dfield.desc
         p.image = ptr(image)
         p.stats = ptr(self._stats)
-        need = N.load().vcb_frame_workspace_bytes(W * H, p.max_iterations)
+        need = N.load().vcb_frame_workspace_bytes(W * p.cam.rows, p.max_iterations)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         p.workspace = ptr(self._ws)
@@ -198,8 +213,9 @@ class RenderSession:
         """Render + maintenance on the session stream; returns the device image
         (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame."""
         W, H = int(self.camera.width), int(self.camera.height)
-        if self._img is None or self._img.shape != (H, W, 4):
-            self._img = torch.empty((H, W, 4), dtype=torch.float32, device=self.device)
+        R = self._band_rows(H)
+        if self._img is None or self._img.shape != (R, W, 4):
+            self._img = torch.empty((R, W, 4), dtype=torch.float32, device=self.device)
         img = self._img
         with torch.cuda.stream(self.stream):
             self._stats.zero_()
@@ -246,6 +262,34 @@ class RenderSession:
             host.copy_(img, non_blocking=True)
         rec = self.collect_record(t0)
         return host.numpy(), rec
+
+    def march_kernel_time(self):
+        """(ms, launches) of the ray-march kernel in the last timing=True frame."""
+        ms = C.c_double(0.0)
+        n = C.c_int64(0)
+        it = int(self.last_frame_stats.get("iterations", 0)) + 1
+        N.call("vcb_march_timing", it, C.byref(ms), C.byref(n))
+        return ms.value, n.value
+
+    def export_state(self):
+        """Full device state as host arrays (tables, pool, owners, stamps, requests,
+        staged loader batch): lets another implementation resume this session."""
+        self.stream.synchronize()
+        c = self.cache
+        d = c.dump()
+        st = d["state"]
+        b3 = c.config.brick_size ** 3
+        n = st["n_staged"]
+        d["pool"] = c.pool.cpu().numpy()
+        d["next_free"] = st["next_free"]
+        d["loaded_total"] = st["loaded_total"]
+        keys = c.staged_keys[:n].cpu().numpy()
+        offs = np.asarray(c.layout.offsets, dtype=np.int64)
+        l = np.searchsorted(offs, keys, side="right") - 1
+        d["staged_keys"] = np.stack([l, keys - offs[l]], axis=1).reshape(-1, 2)
+        d["staged_data"] = c.staging[: n * b3].cpu().numpy().reshape(n, b3)
+        d["session_frame"] = self.frame
+        return d
 
     def debug_state(self):
         """Reference-shaped per-frame state (tables, owner, stamps, requests, batch, reports)."""

@@ -1,0 +1,41 @@
+"""Device pow used by shade ((1-alpha)**ratio, kernels.py:348).
+
+The reference evaluates it with glibc's pow.  That pow is not correctly rounded:
+it misrounds ~7e-4 of these inputs by 1 ulp (verified against 50-digit decimal
+arithmetic).  The device pow is double-double and correctly rounded, so it
+agrees with glibc everywhere glibc is right and differs by exactly 1 ulp where
+glibc is wrong."""
+
+from decimal import Decimal, getcontext
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_shade_pow_is_correctly_rounded_and_within_1ulp_of_libm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_18001_b200 import _native as N
+    from paper_2504_18001_b200.device import ptr
+
+    rng = np.random.default_rng(0)
+    n = 1 << 22
+    alpha = np.concatenate([rng.uniform(1e-4, 1.0, n // 2), 10 ** rng.uniform(-6, 0, n // 2)])
+    x = np.maximum(1.0 - alpha, 1e-12)
+    y = np.concatenate([rng.uniform(1e-3, 16.0, n // 2), rng.uniform(0.5, 1.5, n // 2)])
+    want = np.power(x, y)
+    tx, ty = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    out = torch.empty_like(tx)
+    N.call("vcb_debug_pow", n, ptr(tx), ptr(ty), ptr(out), 0)
+    got = out.cpu().numpy()
+    ulps = np.abs(got.view(np.int64) - want.view(np.int64))
+    assert ulps.max() <= 1, f"max {ulps.max()} ulp from libm"
+    assert float((ulps != 0).mean()) <= 2e-3
+    getcontext().prec = 50
+    bad = np.flatnonzero(ulps)[:200]
+    for i in bad:
+        cr = float(Decimal(float(x[i])) ** Decimal(float(y[i])))
+        assert got[i] == cr, (x[i], y[i], got[i], want[i], cr)

@@ -40,7 +40,15 @@ def _replay_gpu(name, ops, ci):
     ret = fn(*args)
     for ai in range(len(args)):
         if f"{name}{ci}_out{ai}" in ops:
-            np.testing.assert_array_equal(args[ai], ops[f"{name}{ci}_out{ai}"], err_msg=f"{name}{ci} arg {ai}")
+            want = ops[f"{name}{ci}_out{ai}"]
+            if name == "shade" and ai in (7, 8):
+                # color/trans go through 1-(1-a)^r (kernels.py:348).  glibc's pow misrounds
+                # ~7e-4 of these inputs (checked against 50-digit decimal); the device pow is
+                # correctly rounded, and 1-pow cancels, so allow a 1e-11 relative f64 gap
+                # here (the f32 image and every cache decision stay identical)
+                np.testing.assert_allclose(args[ai], want, rtol=1e-11, atol=0, err_msg=f"{name}{ci} arg {ai}")
+            else:
+                np.testing.assert_array_equal(args[ai], want, err_msg=f"{name}{ci} arg {ai}")
     if f"{name}{ci}_ret" in ops:
         np.testing.assert_array_equal(np.asarray(ret), ops[f"{name}{ci}_ret"])
 
