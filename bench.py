@@ -260,10 +260,15 @@ def main():
         return img, t0
 
     # warm-up (cold cache fills; untimed)
+    verbose = bool(os.environ.get("CINR_BENCH_VERBOSE"))
     for f in range(args.warmup):
         img, t0 = frame_device(f)
-        sess.collect_record(t0)
-        parallel.gather_frame(ctx, img, st)
+        parallel.gather_frame(ctx, img, st, args.res)
+        rec = sess.collect_record(t0)
+        if verbose:
+            print(f"warm {f}: {rec.wall_s * 1e3:.2f} ms samples {rec.samples} miss {rec.true_misses} "
+                  f"fb {rec.fallback_hits} it {sess.last_frame_stats.get('iterations')} "
+                  f"rays {sess.last_frame_stats.get('rays')} occ {rec.occupancy:.3f}", file=sys.stderr)
     torch.cuda.synchronize()
 
     # ---- timed: device-resident frames, one CUDA event pair per frame on the session stream
@@ -280,7 +285,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             img, t0 = frame_device(f)
-            parallel.gather_frame(ctx, img, st)
+            parallel.gather_frame(ctx, img, st, args.res)
             e1.record(st)
             rec = sess.collect_record(t0)
             launches += N.load().vcb_last_launch_count()
@@ -289,6 +294,9 @@ def main():
             times.append(parallel.max_over_ranks(ctx, ms))
             samples += rec.samples
             recs.append(rec)
+            if verbose:
+                print(f"timed {f}: {ms:.3f} ms samples {rec.samples} miss {rec.true_misses} "
+                      f"it {sess.last_frame_stats.get('iterations')}", file=sys.stderr)
             km, kn = sess.march_kernel_time()
             march_ms += km
             march_launches += kn
@@ -312,7 +320,7 @@ def main():
                 img_h, rec = sess.render_frame()
             else:
                 img = sess.render_frame_device()
-                full = parallel.gather_frame(ctx, img, st)
+                full = parallel.gather_frame(ctx, img, st, args.res)
                 img_h = full.cpu().numpy() if ctx.rank == 0 else None
                 rec = sess.collect_record(t0)
             walls.append(parallel.max_over_ranks(ctx, (time.perf_counter() - t0) * 1000.0))

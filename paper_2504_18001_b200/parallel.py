@@ -62,19 +62,22 @@ def gather_rows(ctx: Ctx, band: torch.Tensor, height: int) -> torch.Tensor:
     pad = torch.zeros((per, W, Cc), dtype=band.dtype, device=band.device)
     pad[: band.shape[0]] = band
     out = torch.empty((ctx.world * per, W, Cc), dtype=band.dtype, device=band.device)
-    dist.all_gather_into_tensor(out, pad)
+    if ctx.backend == "nccl":
+        dist.all_gather_into_tensor(out, pad)
+    else:
+        dist.all_gather(list(out.view(ctx.world, per, W, Cc).unbind(0)), pad)
     # out[r*per + j] holds film row r + j*world
     full = out.view(ctx.world, per, W, Cc).transpose(0, 1).reshape(per * ctx.world, W, Cc)
     return full[:height]
 
 
-def gather_frame(ctx: Ctx, img: torch.Tensor, stream=None) -> torch.Tensor:
+def gather_frame(ctx: Ctx, img: torch.Tensor, stream=None, height=None) -> torch.Tensor:
+    """NCCL all-gather of this frame's row bands, ordered on the render stream."""
     if ctx.world == 1:
         return img
-    with torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream()):
-        H = int(os.environ.get("CINR_FRAME_H", "0")) or None
-        height = H if H is not None else img.shape[0] * ctx.world
-        return gather_rows(ctx, img, height)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        return gather_rows(ctx, img, height if height is not None else img.shape[0] * ctx.world)
 
 
 def barrier(ctx: Ctx):
