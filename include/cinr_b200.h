@@ -156,7 +156,8 @@ typedef struct {
     VcbFrameStats *stats;    /* device */
     void *workspace;
     int64_t workspace_bytes;
-    int64_t reserved_;
+    int32_t impl;            /* 0 = persistent chained march (default), 1 = per-iteration wavefront */
+    int32_t pad2_;
 } VcbFrameParams;
 
 typedef struct {

@@ -22,6 +22,7 @@ INCLUDE = PKG.parent / "include"
 SOURCES = {
     "capi.cu": [],
     "march.cu": ["-fmad=false"],
+    "chain.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
 }

@@ -324,13 +324,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
     }
 }
 
+template <int kInr>
 __global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* keys, const int64_t* n_keys_dev,
                                     int max_keys, float* out, int* nonfinite) {
     extern __shared__ float smem[];
     MlpSmem m;
     const long long nk = *n_keys_dev;
     if (nk == 0) return;
-    const bool fast = F.kind == 0 && inr_is_default(F);
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
         __syncthreads();
@@ -353,8 +353,8 @@ __global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* k
         ny = ny < G.dims[1] - 1 ? ny : G.dims[1] - 1;
         nz = nz < G.dims[2] - 1 ? nz : G.dims[2] - 1;
         int bad = 0;
-        out[t] = field_eval(F, ((double)nx + 0.5) / (double)G.dims[0], ((double)ny + 0.5) / (double)G.dims[1],
-                            ((double)nz + 0.5) / (double)G.dims[2], m, fast, &bad);
+        out[t] = field_eval<kInr>(F, ((double)nx + 0.5) / (double)G.dims[0], ((double)ny + 0.5) / (double)G.dims[1],
+                                   ((double)nz + 0.5) / (double)G.dims[2], m, &bad);
         if (bad) *nonfinite = 1;
     }
 }
@@ -407,12 +407,11 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     k_select<<<1, kSelThreads, 0, st>>>(P, w);
     // 4. fulfill into the staging slab (inserted at the next maintenance)
     const int sm = mlp_smem_bytes(P.field);
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_decode_bricks_dev, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
-    k_decode_bricks_dev<<<grid_for((int64_t)P.max_requests * b3, 128, 8), 128, sm, st>>>(
-        P.field, P.geom, P.staged_keys,
-        (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged)), P.max_requests, P.staging,
-        w.nonfinite);
+    const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
+    const int64_t* nst = (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged));
+    CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
+                      P.max_requests, P.staging, w.nonfinite);
     k_post_decode<<<1, 1, 0, st>>>(P, w);
     g_launches += 6;
     return check_launch("maintenance");

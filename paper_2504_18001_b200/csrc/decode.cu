@@ -15,11 +15,11 @@ __device__ __forceinline__ long long brick_origin(long long idx, long long b, in
     return idx > 0 ? o - 1 : o;
 }
 
+template <int kInr>
 __global__ void k_field_bricks(VcbField F, VcbBrickGeom G, int64_t n_keys, const int64_t* __restrict__ keys,
                                float* __restrict__ out, int32_t* nonfinite) {
     extern __shared__ float smem[];
     MlpSmem m;
-    const bool fast = F.kind == 0 && inr_is_default(F);
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
         __syncthreads();
@@ -46,23 +46,23 @@ __global__ void k_field_bricks(VcbField F, VcbBrickGeom G, int64_t n_keys, const
         const double py = ((double)ny + 0.5) / (double)G.dims[1];
         const double pz = ((double)nz + 0.5) / (double)G.dims[2];
         int bad = 0;
-        out[t] = field_eval(F, px, py, pz, m, fast, &bad);
+        out[t] = field_eval<kInr>(F, px, py, pz, m, &bad);
         if (bad) *nonfinite = 1;
     }
 }
 
+template <int kInr>
 __global__ void k_field_points(VcbField F, int64_t n, const double* __restrict__ pos, float* __restrict__ out,
                                int32_t* nonfinite) {
     extern __shared__ float smem[];
     MlpSmem m;
-    const bool fast = F.kind == 0 && inr_is_default(F);
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
         __syncthreads();
     }
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         int bad = 0;
-        out[i] = field_eval(F, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], m, fast, &bad);
+        out[i] = field_eval<kInr>(F, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], m, &bad);
         if (bad) *nonfinite = 1;
     }
 }
@@ -70,12 +70,12 @@ __global__ void k_field_points(VcbField F, int64_t n, const double* __restrict__
 // macrocell.py:49-74: lattice values at voxel centres ((i+0.5)/V), per cell the
 // min/max over the cell dilated by one voxel.  One CTA per cell; the lattice is
 // decoded on the fly (never materialised: 4096^3 would be 275 GB).
+template <int kInr>
 __global__ void k_macro_minmax(VcbField F, long long vx, long long vy, long long vz, long long cell, long long gx,
                                long long gy, long long gz, float* vmin, float* vmax) {
     extern __shared__ float smem[];
     __shared__ float rmin[32], rmax[32];
     MlpSmem m;
-    const bool fast = F.kind == 0 && inr_is_default(F);
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
         __syncthreads();
@@ -93,8 +93,8 @@ __global__ void k_macro_minmax(VcbField F, long long vx, long long vy, long long
             if (F.kind == 1) {
                 v = __ldg(F.lattice + (z * vy + y) * vx + x);
             } else {
-                v = field_eval(F, ((double)x + 0.5) / (double)vx, ((double)y + 0.5) / (double)vy,
-                               ((double)z + 0.5) / (double)vz, m, fast, nullptr);
+                v = field_eval<kInr>(F, ((double)x + 0.5) / (double)vx, ((double)y + 0.5) / (double)vy,
+                                      ((double)z + 0.5) / (double)vz, m, nullptr);
             }
             lo = fminf(lo, v);
             hi = fmaxf(hi, v);
@@ -131,10 +131,6 @@ int mlp_smem_bytes(const VcbField& F) {
     return (nw + nb) * (int)sizeof(float);
 }
 
-template <typename K>
-static void allow_smem(K kernel, int bytes) {
-    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
 
 }  // namespace cinr
 
@@ -144,8 +140,8 @@ extern "C" int32_t vcb_field_points(const VcbField* f, int64_t n, const double* 
                                     void* stream) {
     if (n <= 0) return 0;
     const int sm = mlp_smem_bytes(*f);
-    allow_smem(k_field_points, sm);
-    k_field_points<<<grid_for(n, 128, 8), 128, sm, (cudaStream_t)stream>>>(*f, n, pos, out, nonfinite);
+    const int g = grid_for(n, 128, 8);
+    CINR_DISPATCH_INR(*f, k_field_points, g, 128, sm, (cudaStream_t)stream, *f, n, pos, out, nonfinite);
     return check_launch("field_points");
 }
 
@@ -153,10 +149,9 @@ extern "C" int32_t vcb_field_bricks(const VcbField* f, const VcbBrickGeom* g, in
                                     float* out, int32_t* nonfinite, void* stream) {
     if (n_keys <= 0) return 0;
     const int sm = mlp_smem_bytes(*f);
-    allow_smem(k_field_bricks, sm);
     const int64_t total = n_keys * g->b * g->b * g->b;
-    k_field_bricks<<<grid_for(total, 128, 8), 128, sm, (cudaStream_t)stream>>>(*f, *g, n_keys, keys, out,
-                                                                                 nonfinite);
+    const int gr = grid_for(total, 128, 8);
+    CINR_DISPATCH_INR(*f, k_field_bricks, gr, 128, sm, (cudaStream_t)stream, *f, *g, n_keys, keys, out, nonfinite);
     return check_launch("field_bricks");
 }
 
@@ -164,10 +159,9 @@ extern "C" int32_t vcb_macro_minmax(const VcbField* f, const int64_t* dims, int6
                                     void* stream) {
     const long long gx = (dims[0] + cell - 1) / cell, gy = (dims[1] + cell - 1) / cell, gz = (dims[2] + cell - 1) / cell;
     const int sm = mlp_smem_bytes(*f);
-    allow_smem(k_macro_minmax, sm);
     long long cells = gx * gy * gz;
     int grid = (int)(cells < (long long)device_sms() * 16 ? cells : (long long)device_sms() * 16);
-    k_macro_minmax<<<grid, 256, sm, (cudaStream_t)stream>>>(*f, dims[0], dims[1], dims[2], cell, gx, gy, gz, vmin,
-                                                            vmax);
+    CINR_DISPATCH_INR(*f, k_macro_minmax, grid, 256, sm, (cudaStream_t)stream, *f, dims[0], dims[1], dims[2], cell, gx,
+                      gy, gz, vmin, vmax);
     return check_launch("macro_minmax");
 }

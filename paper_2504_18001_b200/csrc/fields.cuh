@@ -163,20 +163,24 @@ static __device__ __noinline__ float inr_generic(const VcbField& F, double x, do
     return zo < 0.0f ? 0.0f : (zo > 1.0f ? 1.0f : zo);
 }
 
-__device__ __forceinline__ bool inr_is_default(const VcbField& F) {
+__host__ __device__ __forceinline__ bool inr_is_default(const VcbField& F) {
     return F.levels == 8 && F.feats == 2 && F.n_layers == 3 && F.widths[0] == 16 && F.widths[1] == 32 &&
            F.widths[2] == 32 && F.widths[3] == 1;
 }
 
-__device__ __forceinline__ float inr_eval(const VcbField& F, double x, double y, double z, const MlpSmem& m,
-                                          bool fast) {
-    if (fast) {
+// kFast: the default 8x2 -> 32 -> 32 -> 1 network, fully in registers; the
+// generic path uses local arrays (a per-thread stack), so it is only compiled
+// into the kernel variants that need it.
+template <bool kFast>
+__device__ __forceinline__ float inr_eval(const VcbField& F, double x, double y, double z, const MlpSmem& m) {
+    if constexpr (kFast) {
         float feat[16];
 #pragma unroll
         for (int l = 0; l < 8; l++) encode_level<2>(F, l, x, y, z, feat + 2 * l);
         return mlp_2h<16, 32>(feat, m, F.out_sigmoid);
+    } else {
+        return inr_generic(F, x, y, z, m);
     }
-    return inr_generic(F, x, y, z, m);
 }
 
 // fields.py:165-199 trilinear_lattice via RawLatticeField._evaluate (u = pos*dims - 0.5)
@@ -224,18 +228,40 @@ __device__ __forceinline__ float procedural_eval(int kind, double x, double y, d
     return __double2float_rn(v);
 }
 
+// kInr: 0 = field is not an INR (no MLP code compiled in), 1 = default INR
+// (register-resident fast path), 2 = any other INR shape (generic path).
+template <int kInr>
 __device__ __forceinline__ float field_eval(const VcbField& F, double x, double y, double z, const MlpSmem& m,
-                                            bool fast, int* nonfinite) {
-    if (F.kind == 0) {
-        float v = inr_eval(F, x, y, z, m, fast);
+                                            int* nonfinite) {
+    if constexpr (kInr != 0) {
+        float v = inr_eval<kInr == 1>(F, x, y, z, m);
         if (!isfinite(v)) {
             if (nonfinite) *nonfinite = 1;
         }
         if (F.clip01) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
         return v;
+    } else {
+        if (F.kind == 1) return lattice_eval(F, x, y, z);
+        return procedural_eval(F.proc, x, y, z);
     }
-    if (F.kind == 1) return lattice_eval(F, x, y, z);
-    return procedural_eval(F.proc, x, y, z);
 }
+
+__host__ __device__ __forceinline__ int inr_mode(const VcbField& F) {
+    return F.kind != 0 ? 0 : (inr_is_default(F) ? 1 : 2);
+}
+
+// launch helper: KERNEL is a template name taking <int kInr>
+#define CINR_DISPATCH_INR(F, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                                   \
+    do {                                                                                               \
+        switch (inr_mode(F)) {                                                                         \
+            case 1: KERNEL<1><<<(GRID), (BLOCK), (SMEM), (STREAM)>>>(__VA_ARGS__); break;              \
+            case 2:                                                                                    \
+                if ((SMEM) > 48 * 1024)                                                                \
+                    cudaFuncSetAttribute(KERNEL<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (SMEM)); \
+                KERNEL<2><<<(GRID), (BLOCK), (SMEM), (STREAM)>>>(__VA_ARGS__);                          \
+                break;                                                                                 \
+            default: KERNEL<0><<<(GRID), (BLOCK), (SMEM), (STREAM)>>>(__VA_ARGS__); break;             \
+        }                                                                                              \
+    } while (0)
 
 }  // namespace cinr

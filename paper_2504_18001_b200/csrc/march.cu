@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kTile) k_march_iter(VcbFrameParams p, FrameWs 
                     uint32_t s = (k == 0) ? lane_seed(p.rng_base, (u64)j) : w.rng[j];
                     s = xorshift32(s);
                     w.rng[j] = s;
-                    u = __ddiv_rn((double)s, 4294967296.0);
+                    u = DMUL((double)s, 2.3283064365386963e-10);  // / 2^32, exact
                 }
                 double dist = a.tmid;
                 if (p.paged_dist) {
@@ -264,9 +264,9 @@ __global__ void __launch_bounds__(kTile) k_march_iter(VcbFrameParams p, FrameWs 
                     double nx = clampd(DSUB(DMUL(a.px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
                     double ny = clampd(DSUB(DMUL(a.py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
                     double nz = clampd(DSUB(DMUL(a.pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
-                    i64 bx = clampi((i64)floor(__ddiv_rn(DADD(nx, 1.0), (double)span)), 0, p.probe.grid[rq][0] - 1);
-                    i64 by = clampi((i64)floor(__ddiv_rn(DADD(ny, 1.0), (double)span)), 0, p.probe.grid[rq][1] - 1);
-                    i64 bz = clampi((i64)floor(__ddiv_rn(DADD(nz, 1.0), (double)span)), 0, p.probe.grid[rq][2] - 1);
+                    i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, p.probe.grid[rq][0] - 1);
+                    i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, p.probe.grid[rq][1] - 1);
+                    i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, p.probe.grid[rq][2] - 1);
                     i64 key = p.probe.offset[rq] + bx + p.probe.grid[rq][0] * (by + p.probe.grid[rq][1] * bz);
                     warp_aggregated_add(p.miss_count, key);
                 }
@@ -306,12 +306,12 @@ __global__ void __launch_bounds__(kTile) k_march_iter(VcbFrameParams p, FrameWs 
 
 // True misses of iteration k: infer through the field (sampler.py:145-154 with
 // clamp_normalized, 119-120), then shade the ray sitting at output slot j.
+template <int kInr>
 __global__ void k_miss_shade(VcbFrameParams p, FrameWs w, int k) {
     extern __shared__ float smem[];
     const int nm = __ldcg(&w.nmiss[k]);
     if (nm == 0) return;
     MlpSmem m;
-    const bool fast = p.field.kind == 0 && inr_is_default(p.field);
     if (p.field.kind == 0) {
         stage_mlp(p.field, smem, m);
         __syncthreads();
@@ -322,7 +322,7 @@ __global__ void k_miss_shade(VcbFrameParams p, FrameWs w, int k) {
         double x = clampd(w.mq_pos[3 * q], 0.0, hi);
         double y = clampd(w.mq_pos[3 * q + 1], 0.0, hi);
         double z = clampd(w.mq_pos[3 * q + 2], 0.0, hi);
-        float v = field_eval(p.field, x, y, z, m, fast, &w.ctr->nonfinite);
+        float v = field_eval<kInr>(p.field, x, y, z, m, &w.ctr->nonfinite);
         const int j = w.mq_slot[q];
         const int32_t id = out.id[j];
         double cr = out.col[3 * j], cg = out.col[3 * j + 1], cb = out.col[3 * j + 2], tr = out.tr[j];
@@ -373,8 +373,13 @@ __global__ void k_frame_stats(VcbFrameParams p, FrameWs w, int kmax) {
 
 using namespace cinr;
 
+int64_t chain_ws_bytes(int64_t npix, int max_it);
+int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches);
+
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
-    return frame_ws_layout(max_rays, max_iterations, nullptr, nullptr);
+    const int64_t a = frame_ws_layout(max_rays, max_iterations, nullptr, nullptr);
+    const int64_t b = chain_ws_bytes(max_rays, max_iterations);
+    return a > b ? a : b;
 }
 
 extern "C" int32_t vcb_raygen_pass(int64_t n, const double* base, const double* rot, const double* origin,
@@ -452,6 +457,11 @@ static unsigned long long* mapped_live(int n, unsigned long long** dev) {
 extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     const VcbFrameParams& p = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
+    if (p.impl == 0) {
+        if ((int64_t)p.cam.width * p.cam.rows == 0) return 0;
+        g_ev_used = 0;
+        return launch_chain_frame(p, st, &g_launches);
+    }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
     FrameWs w;
@@ -476,8 +486,7 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
             nb += p.field.widths[L + 1];
         }
         smem_mlp = (nw + nb) * (int)sizeof(float);
-        if (smem_mlp > 48 * 1024)
-            cudaFuncSetAttribute(k_miss_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mlp);
+
     }
     // Chunks of iterations are queued back to back; before queueing chunk c+1 the
     // host waits for chunk c-1 and stops once its last live count (tagged with this
@@ -504,7 +513,7 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
             if (p.timing) cudaEventRecord(g_ev[2 * k], st);
             k_march_iter<<<iter_grid, kTile, 0, st>>>(p, w, k, dlive);
             if (p.timing) cudaEventRecord(g_ev[2 * k + 1], st);
-            k_miss_shade<<<sms * 4, 256, smem_mlp, st>>>(p, w, k);
+            CINR_DISPATCH_INR(p.field, k_miss_shade, sms * 4, 256, smem_mlp, st, p, w, k);
             g_launches += 2;
         }
         if (p.timing) g_ev_used = k;

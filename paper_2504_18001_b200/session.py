@@ -104,6 +104,7 @@ class RenderSession:
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
         self.timing = False
+        self.impl = 0  # 0 = persistent chained march, 1 = per-iteration wavefront (cross-check)
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
 
     def set_band(self, row0: int, row_step: int):
@@ -198,6 +199,7 @@ class RenderSession:
         p.max_iterations = int(s.max_iterations)
         p.epoch = _next_epoch()
         p.timing = 1 if self.timing else 0
+        p.impl = self.impl
         p.mu, p.lut = ptr(self._mu), ptr(self._lut)
         p.field = self._dfield.desc
         p.image = ptr(image)

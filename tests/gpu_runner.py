@@ -50,7 +50,7 @@ def macro_from(dims, vmin, vmax, cell=16):
                                    np.ones_like(vmin, dtype=np.float32))
 
 
-def run_gpu_session(name, macro=None, frames=None, debug=True):
+def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0):
     """Yields (frame, img, record, session)."""
     from paper_2504_18001_b200.harness import OrbitTrajectory
     from paper_2504_18001_b200.session import RenderSession
@@ -60,6 +60,7 @@ def run_gpu_session(name, macro=None, frames=None, debug=True):
     traj = OrbitTrajectory((0.5, 0.5, 0.5), spec.get("radius", 2.2), 120, width=spec["res"][0], height=spec["res"][1])
     mg = macro_from(spec["dims"], *macro) if macro is not None else None
     sess = RenderSession(fld, product_tf(spec["tf"]), traj.camera_at(0), product_config(spec), macro=mg, debug=debug)
+    sess.impl = impl
     events = spec.get("events", {})
     for f in range(frames if frames is not None else spec["frames"]):
         ev = events.get(f)

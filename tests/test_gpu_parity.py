@@ -209,3 +209,19 @@ def test_session_vs_oracle_random_scene(seed):
             assert np.abs(img - oimg).max() <= 1e-6
     finally:
         scene_specs.SESSION_SPECS.pop(name, None)
+
+
+def test_chained_and_wavefront_marches_agree():
+    """The persistent chained march and the per-iteration wavefront march are two
+    schedules of the same arithmetic: identical images and cache state."""
+    from gpu_runner import run_gpu_session
+
+    g = load_golden("session_pressure.npz")
+    m = (g["macro_vmin"], g["macro_vmax"])
+    for (f, ia, ra, xa), (_, ib, rb, xb) in zip(run_gpu_session("pressure", macro=m, frames=8, impl=0),
+                                               run_gpu_session("pressure", macro=m, frames=8, impl=1)):
+        assert (ra.samples, ra.true_misses, ra.exact_hits) == (rb.samples, rb.true_misses, rb.exact_hits)
+        np.testing.assert_array_equal(ia, ib)
+        da, db = xa.debug_state(), xb.debug_state()
+        for k in ("tables", "owner", "last_used", "entries", "batch"):
+            np.testing.assert_array_equal(da[k], db[k])
