@@ -446,7 +446,8 @@ int64_t chain_ws_bytes(int64_t npix, int max_it) {
                            &fw, &w);
 }
 
-int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches) {
+int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev,
+                       int* ev_used) {
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
     const int mode = inr_mode(p.field);
@@ -490,7 +491,12 @@ int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
     int Gi = G, mi = max_it;
     unsigned int tg = p.epoch * 16384u;
     void* args[6] = {&pc, &wc, (void*)&nr, &Gi, &mi, &tg};
+    if (ev) cudaEventRecord(ev[0], st);
     cudaError_t e = cudaLaunchCooperativeKernel(chain_kernel(mode), G, kChainThreads, args, smem, st);
+    if (ev) {
+        cudaEventRecord(ev[1], st);
+        *ev_used = 1;
+    }
     if (e != cudaSuccess) return set_error("march_frame: cooperative launch (%d CTAs): %s", G, cudaGetErrorString(e));
     k_chain_stats<<<1, 1, 0, st>>>(p, fw, w);
     *launches = 3;

@@ -373,8 +373,11 @@ __global__ void k_frame_stats(VcbFrameParams p, FrameWs w, int kmax) {
 
 using namespace cinr;
 
+namespace cinr {
 int64_t chain_ws_bytes(int64_t npix, int max_it);
-int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches);
+int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev,
+                       int* ev_used);
+}  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
     const int64_t a = frame_ws_layout(max_rays, max_iterations, nullptr, nullptr);
@@ -460,7 +463,14 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     if (p.impl == 0) {
         if ((int64_t)p.cam.width * p.cam.rows == 0) return 0;
         g_ev_used = 0;
-        return launch_chain_frame(p, st, &g_launches);
+        if (p.timing) {
+            while (g_ev.size() < 2) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                g_ev.push_back(e);
+            }
+        }
+        return launch_chain_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
