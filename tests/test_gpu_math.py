@@ -21,12 +21,16 @@ def test_shade_pow_is_correctly_rounded_and_within_1ulp_of_libm():
     from paper_2504_18001_b200 import _native as N
     from paper_2504_18001_b200.device import ptr
 
+    import math
+
     rng = np.random.default_rng(0)
-    n = 1 << 22
+    n = 1 << 18
     alpha = np.concatenate([rng.uniform(1e-4, 1.0, n // 2), 10 ** rng.uniform(-6, 0, n // 2)])
     x = np.maximum(1.0 - alpha, 1e-12)
     y = np.concatenate([rng.uniform(1e-3, 16.0, n // 2), rng.uniform(0.5, 1.5, n // 2)])
-    want = np.power(x, y)
+    # glibc pow through math.pow (what numba's `**` lowers to); np.power may use an
+    # AVX-512 SVML kernel on the GPU host and is not the reference's pow
+    want = np.array([math.pow(a, b) for a, b in zip(x.tolist(), y.tolist())])
     tx, ty = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
     out = torch.empty_like(tx)
     N.call("vcb_debug_pow", n, ptr(tx), ptr(ty), ptr(out), 0)
