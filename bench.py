@@ -359,7 +359,7 @@ def main():
                        "macro": msrc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(),
-                         "kernel": "k_chain_march (persistent: advance+rank+probe+shade+miss inference, all iterations)",
+                         "kernel": "k_wave_march (persistent cooperative: all iterations; advance+rank+probe+shade+miss inference)",
                          "algorithmic_bytes": f"{BYTES_PER_SAMPLE} B/sample x samples per launch",
                          "launches": march_launches, "avg_launch_us": 1000.0 * march_ms / max(march_launches, 1),
                          "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,

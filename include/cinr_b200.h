@@ -156,7 +156,7 @@ typedef struct {
     VcbFrameStats *stats;    /* device */
     void *workspace;
     int64_t workspace_bytes;
-    int32_t impl;            /* 0 = persistent chained march (default), 1 = per-iteration wavefront */
+    int32_t impl;            /* 0 = persistent wavefront (default), 1 = launch per iteration, 2 = chained CTAs */
     int32_t pad2_;
 } VcbFrameParams;
 

@@ -23,6 +23,7 @@ SOURCES = {
     "capi.cu": [],
     "march.cu": ["-fmad=false"],
     "chain.cu": ["-fmad=false"],
+    "wave.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
 }

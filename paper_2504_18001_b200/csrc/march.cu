@@ -304,6 +304,12 @@ __global__ void __launch_bounds__(kTile) k_march_iter(VcbFrameParams p, FrameWs 
     }
 }
 
+void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st) {
+    const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
+    k_raygen_frame<<<grid_for(npix, 256), 256, 0, st>>>(p, w);
+    k_compact_rays<<<device_sms() * 4, kTile, 0, st>>>(p, w);
+}
+
 // True misses of iteration k: infer through the field (sampler.py:145-154 with
 // clamp_normalized, 119-120), then shade the ray sitting at output slot j.
 template <int kInr>
@@ -377,6 +383,7 @@ namespace cinr {
 int64_t chain_ws_bytes(int64_t npix, int max_it);
 int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev,
                        int* ev_used);
+int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
@@ -460,7 +467,7 @@ static unsigned long long* mapped_live(int n, unsigned long long** dev) {
 extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     const VcbFrameParams& p = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
-    if (p.impl == 0) {
+    if (p.impl == 0 || p.impl == 2) {
         if ((int64_t)p.cam.width * p.cam.rows == 0) return 0;
         g_ev_used = 0;
         if (p.timing) {
@@ -470,7 +477,8 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
                 g_ev.push_back(e);
             }
         }
-        return launch_chain_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
+        if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
+        return launch_wave_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;

@@ -211,15 +211,17 @@ def test_session_vs_oracle_random_scene(seed):
         scene_specs.SESSION_SPECS.pop(name, None)
 
 
-def test_chained_and_wavefront_marches_agree():
-    """The persistent chained march and the per-iteration wavefront march are two
-    schedules of the same arithmetic: identical images and cache state."""
+@pytest.mark.parametrize("other", [1, 2])
+def test_march_schedules_agree(other):
+    """The persistent wavefront (default), the launch-per-iteration wavefront and
+    the chained-CTA march are schedules of the same arithmetic: identical images
+    and cache state."""
     from gpu_runner import run_gpu_session
 
     g = load_golden("session_pressure.npz")
     m = (g["macro_vmin"], g["macro_vmax"])
     for (f, ia, ra, xa), (_, ib, rb, xb) in zip(run_gpu_session("pressure", macro=m, frames=8, impl=0),
-                                               run_gpu_session("pressure", macro=m, frames=8, impl=1)):
+                                               run_gpu_session("pressure", macro=m, frames=8, impl=other)):
         assert (ra.samples, ra.true_misses, ra.exact_hits) == (rb.samples, rb.true_misses, rb.exact_hits)
         np.testing.assert_array_equal(ia, ib)
         da, db = xa.debug_state(), xb.debug_state()
