@@ -21,6 +21,7 @@
 namespace cinr {
 
 constexpr int kWaveThreads = 256;
+constexpr long long kOccMaxCells = 1ll << 18;  // 32 KB of shared memory
 static_assert(kWaveThreads == kTile, "tile = one ray per thread");
 
 struct WaveSmem {
@@ -64,7 +65,25 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
     extern __shared__ unsigned char dsmem[];
     __shared__ WaveSmem sm;
     MlpSmem mlp;
-    if (p.field.kind == 0) stage_mlp(p.field, reinterpret_cast<float*>(dsmem), mlp);
+    int mlp_floats = 0;
+    if (p.field.kind == 0) {
+        int nb;
+        mlp_floats = mlp_param_count(p.field, nb) + nb;
+        stage_mlp(p.field, reinterpret_cast<float*>(dsmem), mlp);
+    }
+    // non-empty-cell bitmask of the macro grid in shared memory (when it fits)
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    uint32_t* occ = nullptr;
+    if (cells <= kOccMaxCells && p.adv.skip_empty) {
+        occ = reinterpret_cast<uint32_t*>(dsmem + ((mlp_floats * 4 + 15) & ~15));
+        const int nwords = (int)((cells + 31) >> 5);
+        for (int wd = threadIdx.x >> 5; wd < nwords; wd += blockDim.x >> 5) {
+            const long long c = (long long)wd * 32 + (threadIdx.x & 31);
+            const unsigned b = __ballot_sync(0xffffffffu, c < cells && __ldg(p.mu + c) > 0.0f);
+            if ((threadIdx.x & 31) == 0) occ[wd] = b;
+        }
+    }
+    __syncthreads();
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0;
     const double ox = p.cam.origin[0], oy = p.cam.origin[1], oz = p.cam.origin[2];
     const int lane = threadIdx.x & 31;
@@ -77,12 +96,9 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
         const LiveBuf out = w.buf[(k + 1) & 1];
         const long long ntiles = (n + kTile - 1) / kTile;
         const unsigned int tag = p.epoch * 16384u + (unsigned int)k;
-        for (;;) {
-            if (threadIdx.x == 0) sm.scan.tile = atomicAdd(&w.ticket[k], 1);
-            if (threadIdx.x == 0) sm.n_miss = 0;
-            __syncthreads();
-            const long long tile = sm.scan.tile;
-            if (tile >= ntiles) break;
+        // static round-robin tiles: CTA c walks c, c+G, c+2G, ... in increasing order,
+        // so every look-back predecessor is either done or being worked on
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const long long i = tile * kTile + threadIdx.x;
             int flag = 0;
             int32_t id = -1;
@@ -100,7 +116,7 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
                     cb = __ldcg(in.col + 3 * i + 2);
                     tr = __ldcg(in.tr + i);
                     flag = advance_one(ox, oy, oz, w.ray_dir[3 * id], w.ray_dir[3 * id + 1], w.ray_dir[3 * id + 2],
-                                       w.ray_ten[id], w.ray_tex[id], cf, ck, p.adv, p.mu, a);
+                                       w.ray_ten[id], w.ray_tex[id], cf, ck, p.adv, p.mu, a, occ);
                     if (!flag) retire_w(p, w.ray_pix[id], cr, cg, cb, tr);
                 }
             }
@@ -237,8 +253,10 @@ int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launc
             nb += p.field.widths[L + 1];
         }
         smem = (nw + nb) * 4;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(wave_kernel(mode), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    if (cells <= kOccMaxCells && p.adv.skip_empty) smem = ((smem + 15) & ~15) + (int)(((cells + 31) >> 5) * 4);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(wave_kernel(mode), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wave_kernel(mode), kWaveThreads, smem);
     if (per_sm < 1) per_sm = 1;
