@@ -55,7 +55,7 @@ inline int64_t frame_ws_layout(int64_t n, int32_t max_it, void* base, FrameWs* w
         off = o + bytes;
         return o;
     };
-    const int64_t tiles = (n + kTile - 1) / kTile + 1;
+    const int64_t tiles = (n + kTile - 1) / kTile + 1 + 8 * 148 * 8;  // + G for even-tile rounding
     size_t o_keep = take((size_t)n);
     size_t o_pix = take((size_t)n * 4);
     size_t o_dir = take((size_t)n * 24);
@@ -72,7 +72,7 @@ inline int64_t frame_ws_layout(int64_t n, int32_t max_it, void* base, FrameWs* w
     size_t o_mqs = take((size_t)n * 4);
     size_t o_mqp = take((size_t)n * 24);
     size_t o_mqd = take((size_t)n * 8);
-    size_t o_st = take((size_t)tiles * 8);
+    size_t o_st = take((size_t)tiles * 16);  // look-back words (wave march: agg + incl)
     size_t o_ctr = take(sizeof(FrameCounters));
     size_t iter_bytes = (size_t)(max_it + 2) * 4 * 3;
     size_t o_it = take(iter_bytes);

@@ -26,8 +26,7 @@ static_assert(kWaveThreads == kTile, "tile = one ray per thread");
 
 struct WaveSmem {
     ScanSmem scan;
-    int n_miss;
-    int miss_tid[kWaveThreads];
+    long long wsum[kWaveThreads / 32];
     unsigned long long cnt[3];
 };
 
@@ -57,6 +56,57 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsig
         __threadfence();
     }
     __syncthreads();
+}
+
+// Rank of each sampling ray of tile (round r, column c) of iteration k.  Every
+// tile publishes its own count (agg) and, once known, its inclusive prefix
+// (incl).  A tile reads, in parallel, the aggs of the c tiles before it in its
+// round plus the incl of the last tile of the previous round: one step instead
+// of a 32-wide walk back through the round.
+__device__ __forceinline__ long long round_scan(int flag, long long tile, int G, unsigned long long* agg,
+                                                unsigned long long* incl, unsigned int tag, WaveSmem& sm,
+                                                long long& rank, long long& total_incl) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int wpre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) sm.scan.warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int wbase = 0, btot = 0;
+#pragma unroll
+    for (int i = 0; i < kWaveThreads / 32; i++) {
+        const int t = sm.scan.warp_tot[i];
+        wbase += (i < warp) ? t : 0;
+        btot += t;
+    }
+    const unsigned long long tagw = (unsigned long long)tag << 32;
+    if (threadIdx.x == 0) st_volatile_u64(agg + tile, tagw | (unsigned long long)btot);
+    const long long r = tile / G, c = tile - r * G, base = r * G;
+    long long acc = 0;
+    for (long long q = threadIdx.x; q < c; q += blockDim.x) {
+        unsigned long long s;
+        do {
+            s = ld_volatile_u64(agg + base + q);
+        } while ((s >> 32) != tag);
+        acc += (long long)(s & 0xFFFFFFFFull);
+    }
+    if (threadIdx.x == blockDim.x - 1 && r > 0) {
+        unsigned long long s;
+        do {
+            s = ld_volatile_u64(incl + base - 1);
+        } while ((s >> 32) != tag);
+        acc += (long long)(s & 0xFFFFFFFFull);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) sm.wsum[warp] = acc;
+    __syncthreads();
+    long long pre = 0;
+#pragma unroll
+    for (int i = 0; i < kWaveThreads / 32; i++) pre += sm.wsum[i];
+    if (threadIdx.x == 0) st_volatile_u64(incl + tile, tagw | (unsigned long long)(pre + btot));
+    rank = pre + wbase + wpre;
+    total_incl = pre + btot;
+    __syncthreads();  // sm reuse by the next tile
+    return pre;
 }
 
 template <int kInr>
@@ -94,18 +144,23 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
         if (n == 0) break;
         const LiveBuf in = w.buf[k & 1];
         const LiveBuf out = w.buf[(k + 1) & 1];
-        const long long ntiles = (n + kTile - 1) / kTile;
+        // even tiles: the iteration's n rays split into G * rounds tiles of <= 256,
+        // so every CTA works the same number of rounds (no partial last round)
+        const int G = gridDim.x;
+        const long long rounds = (n + (long long)kTile * G - 1) / ((long long)kTile * G);
+        const long long ntiles = rounds * G;
         const unsigned int tag = p.epoch * 16384u + (unsigned int)k;
-        // static round-robin tiles: CTA c walks c, c+G, c+2G, ... in increasing order,
-        // so every look-back predecessor is either done or being worked on
-        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const long long i = tile * kTile + threadIdx.x;
+        // static round-robin: CTA c walks tiles c, c+G, c+2G, ... in increasing order,
+        // so every rank predecessor is done or in flight (no deadlock)
+        for (long long tile = blockIdx.x; tile < ntiles; tile += G) {
+            const long long lo = tile * n / ntiles, hi = (tile + 1) * n / ntiles;
+            const long long i = lo + threadIdx.x;
             int flag = 0;
             int32_t id = -1;
             double cf = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, tr = 1.0;
             i64 ck = 0;
             AdvanceOut a;
-            if (i < n) {
+            if (i < hi) {
                 id = __ldcg(in.id + i);
                 if (id >= 0) {
                     const long long cur = __ldcg(in.cur + i);
@@ -120,9 +175,9 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
                     if (!flag) retire_w(p, w.ray_pix[id], cr, cg, cb, tr);
                 }
             }
-            long long j;
-            const uint32_t total = ordered_scan(flag, tile, w.status, tag, sm.scan, j);
-            if (tile == ntiles - 1 && threadIdx.x == kTile - 1) w.live[k + 1] = (int)total;
+            long long j, incl_total;
+            round_scan(flag, tile, G, w.status, w.status + w.max_tiles, tag, sm, j, incl_total);
+            if (tile == ntiles - 1 && threadIdx.x == 0) w.live[k + 1] = (int)incl_total;
             int miss = 0, dead = 0;
             float v = 0.0f;
             if (flag) {
@@ -166,9 +221,9 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
                     }
                 }
             }
-            // true misses of this tile: infer through the field (inputs clamped to
+            // true misses: infer through the field (inputs clamped to
             // [0, nextafter(1,0)], sampler.py:119-120), then shade
-            if (__syncthreads_or(miss)) {
+            {
                 if (miss) {
                     const double hi = 0.99999999999999989;
                     int bad = 0;
