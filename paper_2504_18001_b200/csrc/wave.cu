@@ -175,9 +175,9 @@ __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p
                     if (!flag) retire_w(p, w.ray_pix[id], cr, cg, cb, tr);
                 }
             }
-            long long j, incl_total;
-            round_scan(flag, tile, G, w.status, w.status + w.max_tiles, tag, sm, j, incl_total);
-            if (tile == ntiles - 1 && threadIdx.x == 0) w.live[k + 1] = (int)incl_total;
+            long long j;
+            const uint32_t total = ordered_scan(flag, tile, w.status, tag, sm.scan, j);
+            if (tile == ntiles - 1 && threadIdx.x == kTile - 1) w.live[k + 1] = (int)total;
             int miss = 0, dead = 0;
             float v = 0.0f;
             if (flag) {

@@ -42,4 +42,26 @@ def main(rep, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    import contextlib
+    import io
+    import json
+
+    rep = sys.argv[1]
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        res = main(rep, int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    text = buf.getvalue()
+    print(text)
+    if len(sys.argv) > 3:  # write profiles/<tag>.txt + .json
+        tag = sys.argv[3]
+        open(f"profiles/{tag}.txt", "w").write(text)
+        def num(k):
+            v = res.get(k)
+            return float(v[0].replace(",", "")) if v else None
+        rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rdu = scale.get(res.get("dram__bytes_read.sum", (0, "byte"))[1], 1)
+        wru = scale.get(res.get("dram__bytes_write.sum", (0, "byte"))[1], 1)
+        out = {"report": rep, "dram_bytes_per_launch": (rd * rdu + wr * wru) if rd is not None else None,
+               "metrics": {k: v for k, v in res.items()}}
+        json.dump(out, open(f"profiles/{tag}.json", "w"), indent=1)
