@@ -133,7 +133,7 @@ def measured_peak_hbm():
 
 
 def profiled_traffic():
-    f = ROOT / "profiles" / "ncu_march_iter.json"
+    f = ROOT / "profiles" / "ncu_frame_kernel.json"
     if f.exists():
         try:
             return json.loads(f.read_text()).get("dram_bytes_per_launch")
@@ -143,8 +143,8 @@ def profiled_traffic():
 
 
 # --------------------------------------------------------------------------- CPU arms
-def cpu_oracle_frame_from_state(state, macro, res_frac, frame_idx, volume):
-    """One steady-state frame of the oracle from the GPU session's exact state."""
+def cpu_oracle_frame_from_state(state, macro, res_frac, frame_idx, volume, frames=1):
+    """Steady-state frames of the oracle, resumed from the GPU session's exact state."""
     from oracle import cinr_oracle as O
 
     t, w, b = O.inr_params_from_seed(O.DEFAULT_GRID, O.DEFAULT_MLP)
@@ -153,11 +153,13 @@ def cpu_oracle_frame_from_state(state, macro, res_frac, frame_idx, volume):
     sess = O.OracleSession(fld, O.warm_body_points(0.5, 0.9), cfg, macro_minmax_arrays=macro)
     O.load_session_state(sess, state)
     res = int(1024 * res_frac)
-    pos = O.orbit_camera((0.5, 0.5, 0.5), 2.2, 120, frame_idx)
-    sess.set_camera(pos, (0.5, 0.5, 0.5), (0.0, 1.0, 0.0), 45.0, res, res)
-    t0 = time.perf_counter()
-    img, rec = sess.render_frame()
-    return time.perf_counter() - t0, img, rec
+    wall = 0.0
+    for f in range(frames):
+        pos = O.orbit_camera((0.5, 0.5, 0.5), 2.2, 120, frame_idx + f)
+        sess.set_camera(pos, (0.5, 0.5, 0.5), (0.0, 1.0, 0.0), 45.0, res, res)
+        img, rec = sess.render_frame()
+        wall += rec.wall_s
+    return wall / frames, img, rec
 
 
 def run_reference_arm(args):
@@ -210,7 +212,9 @@ def main():
     ap.add_argument("--res", type=int, default=1024)
     ap.add_argument("--volume", type=int, default=512)
     ap.add_argument("--ref-res", type=int, default=128)
-    ap.add_argument("--cpu-frac", type=float, default=0.25, help="oracle baseline image fraction of --res")
+    ap.add_argument("--cpu-frac", type=float, default=1.0, help="oracle baseline image fraction of --res")
+    ap.add_argument("--cpu-frames", type=int, default=3, help="oracle baseline frames (from the GPU state)")
+    ap.add_argument("--decode-n", type=int, default=1 << 24, help="isolated INR decode batch (0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -336,16 +340,26 @@ def main():
             state = sess.export_state()
             frac = args.cpu_frac
             wall, oimg, orec = cpu_oracle_frame_from_state(state, (mg.value_min, mg.value_max), frac, sess.frame,
-                                                            args.volume)
+                                                            args.volume, args.cpu_frames)
             cores = os.cpu_count() or 1
             cpu = {"value": (frac * frac) / wall, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": (f"1 steady-state frame (orbit frame {sess.frame}) rendered by the oracle port "
-                              f"(C+numpy restatement of voxcache, OpenMP {cores} threads) from the GPU session's exact "
-                              f"cache/request/loader state at {int(args.res * frac)}^2, render+maintenance "
-                              f"{wall:.2f}s, fps scaled by the pixel ratio {frac * frac:.4f}")}
+                   "sample": (f"{args.cpu_frames} frames (orbit frames {sess.frame}..{sess.frame + args.cpu_frames - 1}) "
+                              f"rendered by the oracle port (C+numpy restatement of voxcache, OpenMP {cores} threads), "
+                              f"resumed from the GPU session's exact cache/request/loader state, at "
+                              f"{int(args.res * frac)}^2; mean render+maintenance {wall:.2f}s/frame"
+                              + (f", fps scaled by the pixel ratio {frac * frac:.4f}" if frac != 1.0 else ""))}
         except Exception as exc:  # the baseline is reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
 
+    decode = None
+    if ctx.rank == 0 and args.decode_n > 0:
+        try:
+            sys.path.insert(0, str(ROOT / "tools"))
+            import decode_bench
+
+            decode = decode_bench.run(args.decode_n, reps=3)
+        except Exception as exc:
+            decode = {"error": str(exc)}
     peak, peak_src = measured_peak_hbm()
     achieved = (samples_all * BYTES_PER_SAMPLE) / (march_ms / 1000.0) / 1e9 if march_ms > 0 else None
     if ctx.rank == 0:
@@ -364,7 +378,7 @@ def main():
                          "launches": march_launches, "avg_launch_us": 1000.0 * march_ms / max(march_launches, 1),
                          "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,
                          "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "inr_decode": decode, "clocks": clk.summary(), "gpu_launches": launches,
             "samples_per_frame": samples_all / args.steps,
             "inr_samples_per_frame": float(np.mean([r.true_misses for r in recs])) + 40 * 16 ** 3,
             "hit_rate": 1.0 - sum(r.true_misses for r in recs) / max(1, sum(r.samples for r in recs)),

@@ -213,6 +213,12 @@ int32_t vcb_field_points(const VcbField *f, int64_t n, const double *pos, float 
                          void *stream);
 int32_t vcb_field_bricks(const VcbField *f, const VcbBrickGeom *g, int64_t n_keys, const int64_t *keys,
                          float *out, int32_t *nonfinite, void *stream);
+/* Tensor-core (tcgen05) decoder for the default INR shape (8x2 hash grid,
+ * 16->32->32->1): the same contract as vcb_field_points / vcb_field_bricks. */
+int32_t vcb_inr_points_tc(const VcbField *f, int64_t n, const double *pos, float *out, int32_t *nonfinite,
+                          void *stream);
+int32_t vcb_inr_bricks_tc(const VcbField *f, const VcbBrickGeom *g, int64_t n_keys, const int64_t *keys,
+                          float *out, int32_t *nonfinite, void *stream);
 int32_t vcb_macro_minmax(const VcbField *f, const int64_t *dims, int64_t cell, float *vmin, float *vmax,
                          void *stream);
 

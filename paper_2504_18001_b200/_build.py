@@ -26,6 +26,7 @@ SOURCES = {
     "wave.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
+    "decode_tc.cu": [],
 }
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

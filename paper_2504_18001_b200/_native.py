@@ -102,6 +102,8 @@ _PROTOS = {
     "vcb_debug_pow": (i32, [i64, vp, vp, vp, vp]),
     "vcb_field_points": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),
     "vcb_field_bricks": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
+    "vcb_inr_points_tc": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),
+    "vcb_inr_bricks_tc": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
     "vcb_macro_minmax": (i32, [C.POINTER(VcbField), vp, i64, vp, vp, vp]),
     "vcb_frame_workspace_bytes": (i64, [i64, i32]),
     "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),

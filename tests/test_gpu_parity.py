@@ -227,3 +227,41 @@ def test_march_schedules_agree(other):
         da, db = xa.debug_state(), xb.debug_state()
         for k in ("tables", "owner", "last_used", "entries", "batch"):
             np.testing.assert_array_equal(da[k], db[k])
+
+
+def test_tensor_core_decoder_vs_reference():
+    """tcgen05 MLP decoder (split-fp16, fp32 accumulate in TMEM) against the
+    reference's INR outputs and the CUDA-core decoder."""
+    from gpu_runner import product_inr
+    from paper_2504_18001_b200 import _native as N
+    from paper_2504_18001_b200.cache import BrickLayout
+    from paper_2504_18001_b200.device import device_field, ptr
+
+    g = load_golden("inr.npz")
+    m = product_inr((64, 64, 64))
+    df = device_field(m.as_field())
+    pos = np.concatenate([g["default_pos"], np.random.default_rng(9).random((70000, 3))])
+    tp = _dev(pos)
+    out_tc = torch.empty(len(pos), dtype=torch.float32, device="cuda")
+    out_cc = torch.empty(len(pos), dtype=torch.float32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.call("vcb_inr_points_tc", C.byref(df.desc), len(pos), ptr(tp), ptr(out_tc), ptr(flag), 0)
+    N.call("vcb_field_points", C.byref(df.desc), len(pos), ptr(tp), ptr(out_cc), ptr(flag), 0)
+    tc, cc = out_tc.cpu().numpy(), out_cc.cpu().numpy()
+    n0 = len(g["default_pos"])
+    np.testing.assert_allclose(tc[:n0], g["default_field"], atol=1e-5, rtol=0)
+    np.testing.assert_allclose(tc, cc, atol=1e-5, rtol=0)
+    # brick variant writes the pool layout
+    lay = BrickLayout((64, 64, 64), 16)
+    keys = []
+    refs = []
+    for k in [k for k in g if k.startswith("default_brick_")]:
+        lod = int(k.split("_")[2])
+        idx = [int(c) for c in k.split("_")[3]]
+        keys.append(lay.offsets[lod] + idx[0] + lay.grids[lod][0] * (idx[1] + lay.grids[lod][1] * idx[2]))
+        refs.append(g[k])
+    kt = _dev(np.array(keys, dtype=np.int64))
+    out = torch.empty(len(keys) * 16 ** 3, dtype=torch.float32, device="cuda")
+    geom = lay.geom()
+    N.call("vcb_inr_bricks_tc", C.byref(df.desc), C.byref(geom), len(keys), ptr(kt), ptr(out), ptr(flag), 0)
+    np.testing.assert_allclose(out.cpu().numpy().reshape(len(keys), -1), np.stack(refs), atol=1e-5, rtol=0)
