@@ -156,7 +156,8 @@ typedef struct {
     VcbFrameStats *stats;    /* device */
     void *workspace;
     int64_t workspace_bytes;
-    int32_t impl;            /* 0 = persistent wavefront (default), 1 = launch per iteration, 2 = chained CTAs */
+    int32_t impl;            /* march schedule: 0 = two-phase persistent wavefront (default), 1 = one launch
+                                per iteration, 2 = chained CTAs, 3 = persistent wavefront with look-back */
     int32_t pad2_;
 } VcbFrameParams;
 

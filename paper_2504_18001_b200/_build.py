@@ -24,6 +24,7 @@ SOURCES = {
     "march.cu": ["-fmad=false"],
     "chain.cu": ["-fmad=false"],
     "wave.cu": ["-fmad=false"],
+    "wave2.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
     "decode_tc.cu": [],

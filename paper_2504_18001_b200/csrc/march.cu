@@ -384,6 +384,7 @@ int64_t chain_ws_bytes(int64_t npix, int max_it);
 int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev,
                        int* ev_used);
 int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
+int launch_wave2_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
@@ -467,7 +468,7 @@ static unsigned long long* mapped_live(int n, unsigned long long** dev) {
 extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     const VcbFrameParams& p = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
-    if (p.impl == 0 || p.impl == 2) {
+    if (p.impl != 1) {
         if ((int64_t)p.cam.width * p.cam.rows == 0) return 0;
         g_ev_used = 0;
         if (p.timing) {
@@ -477,8 +478,10 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
                 g_ev.push_back(e);
             }
         }
-        if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
-        return launch_wave_frame(p, st, &g_launches, p.timing ? g_ev.data() : nullptr, &g_ev_used);
+        cudaEvent_t* ev = p.timing ? g_ev.data() : nullptr;
+        if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, ev, &g_ev_used);
+        if (p.impl == 3) return launch_wave_frame(p, st, &g_launches, ev, &g_ev_used);
+        return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;

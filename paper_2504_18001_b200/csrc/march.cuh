@@ -70,7 +70,7 @@ inline int64_t frame_ws_layout(int64_t n, int32_t max_it, void* base, FrameWs* w
     }
     size_t o_rng = take((size_t)n * 4);
     size_t o_mqs = take((size_t)n * 4);
-    size_t o_mqp = take((size_t)n * 24);
+    size_t o_mqp = take((size_t)n * 48);  // miss positions (v1) / advance outputs by slot (two-phase)
     size_t o_mqd = take((size_t)n * 8);
     size_t o_st = take((size_t)tiles * 16);  // look-back words (wave march: agg + incl)
     size_t o_ctr = take(sizeof(FrameCounters));
