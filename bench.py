@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--decode-n", type=int, default=1 << 24, help="isolated INR decode batch (0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", type=int, default=0,
+                    help="march schedule (VcbFrameParams.impl): 0 one-barrier wavefront (default), 4 two-phase, 5 = 0 at 768 threads")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -254,6 +256,7 @@ def main():
                         settings=P.RenderSettings(), seed=0)
     traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=args.res, height=args.res)
     sess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+    sess.impl = args.schedule
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     st = sess.stream
 
@@ -304,6 +307,8 @@ def main():
             km, kn = sess.march_kernel_time()
             march_ms += km
             march_launches += kn
+    if os.environ.get("CINR_TRACE"):
+        Path(os.environ["CINR_TRACE"]).write_text(json.dumps(sess.frame_trace()))
     sess.timing = False
     total_ms = sum(times)
     fps = args.steps / (total_ms / 1000.0)
@@ -373,7 +378,7 @@ def main():
                        "macro": msrc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(),
-                         "kernel": "k_wave_march (persistent cooperative: all iterations; advance+rank+probe+shade+miss inference)",
+                         "kernel": "k_wave3_march (persistent cooperative, one grid barrier per iteration: rank+probe+shade+next advance; queued miss inference)",
                          "algorithmic_bytes": f"{BYTES_PER_SAMPLE} B/sample x samples per launch",
                          "launches": march_launches, "avg_launch_us": 1000.0 * march_ms / max(march_launches, 1),
                          "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,

@@ -156,8 +156,9 @@ typedef struct {
     VcbFrameStats *stats;    /* device */
     void *workspace;
     int64_t workspace_bytes;
-    int32_t impl;            /* march schedule: 0 = two-phase persistent wavefront (default), 1 = one launch
-                                per iteration, 2 = chained CTAs, 3 = persistent wavefront with look-back */
+    int32_t impl;            /* march schedule: 0 = one-barrier persistent wavefront (default), 1 = one launch
+                                per iteration, 2 = chained CTAs, 3 = persistent wavefront with look-back,
+                                4 = two-phase persistent wavefront, 5 = schedule 0 with 768 threads/CTA */
     int32_t pad2_;
 } VcbFrameParams;
 
@@ -229,6 +230,13 @@ int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);
 /* After the stream of a timing=1 frame has completed: summed device time (ms) and
  * count of the first `n_iters` iteration-kernel launches (the ray-march kernel). */
 int32_t vcb_march_timing(int32_t n_iters, double *ms_total, int64_t *launches);
+/* Diagnostics after a timing=1 frame of the default schedule (synchronous): for
+ * iteration k < n (n <= 512) and CTA c < 1024, stamps[(k*1024 + c)*3 + {0,1,2}] =
+ * low 32 bits of %globaltimer after the grid barrier, after the rank scan and when
+ * the CTA finished its phase; live[k+1] = samples of iteration k (live[0] = rays).
+ * Returns the number of iterations copied. */
+int32_t vcb_frame_trace(const void *workspace, int64_t max_rays, int32_t max_iterations, int32_t n,
+                        uint32_t *stamps, int32_t *live);
 /* Kernels launched by this thread's last march_frame + maintenance calls. */
 int64_t vcb_last_launch_count(void);
 int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests);

@@ -25,6 +25,7 @@ SOURCES = {
     "chain.cu": ["-fmad=false"],
     "wave.cu": ["-fmad=false"],
     "wave2.cu": ["-fmad=false"],
+    "wave3.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
     "decode_tc.cu": [],

@@ -385,10 +385,14 @@ int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
                        int* ev_used);
 int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 int launch_wave2_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
+int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
+                       int nt);
+int64_t wave3_ws_bytes(int64_t npix, int max_it);
+int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned int* out, int* live);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
-    const int64_t a = frame_ws_layout(max_rays, max_iterations, nullptr, nullptr);
+    const int64_t a = wave3_ws_bytes(max_rays, max_iterations);  // includes frame_ws_layout
     const int64_t b = chain_ws_bytes(max_rays, max_iterations);
     return a > b ? a : b;
 }
@@ -481,7 +485,9 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         cudaEvent_t* ev = p.timing ? g_ev.data() : nullptr;
         if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 3) return launch_wave_frame(p, st, &g_launches, ev, &g_ev_used);
-        return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
+        if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
+        if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768);
+        return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
@@ -571,3 +577,9 @@ extern "C" int32_t vcb_march_timing(int32_t n_iters, double* ms_total, int64_t* 
 }
 
 extern "C" int64_t vcb_last_launch_count(void) { return g_launches; }
+
+// Diagnostics of the last timing=1 frame of the default schedule.
+extern "C" int32_t vcb_frame_trace(const void* workspace, int64_t max_rays, int32_t max_iterations, int32_t n,
+                                   uint32_t* stamps, int32_t* live) {
+    return wave3_trace(workspace, max_rays, max_iterations, n, stamps, live);
+}

@@ -104,7 +104,7 @@ class RenderSession:
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
         self.timing = False
-        self.impl = 0  # 0 = persistent chained march, 1 = per-iteration wavefront (cross-check)
+        self.impl = 0  # march schedule (VcbFrameParams.impl): 0 = one-barrier persistent wavefront
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
 
     def set_band(self, row0: int, row_step: int):
@@ -272,6 +272,25 @@ class RenderSession:
         it = int(self.last_frame_stats.get("iterations", 0)) + 1
         N.call("vcb_march_timing", it, C.byref(ms), C.byref(n))
         return ms.value, n.value
+
+    def frame_trace(self):
+        """Per-iteration diagnostics of the last timing=True frame (default schedule):
+        per CTA, ns from the iteration's earliest barrier exit to barrier exit, scan
+        done and phase done; plus samples per iteration."""
+        self.stream.synchronize()
+        it = min(int(self.last_frame_stats.get("iterations", 0)), 512)
+        W = int(self.camera.width)
+        rows = self._band_rows(int(self.camera.height))
+        max_it = int(self.config.settings.max_iterations)
+        st = np.zeros((max(it, 1), 1024, 3), np.uint32)
+        lv = np.zeros(it + 2, np.int32)
+        n = N.load().vcb_frame_trace(ptr(self._ws), W * rows, max_it, it, st.ctypes.data, lv.ctypes.data)
+        G = N.load().vcb_device_sm_count()
+        st = st[:n, :G].astype(np.int64)
+        t0 = st[:, :, 0].min(axis=1, keepdims=True)
+        rel = ((st - t0[:, :, None]) % (1 << 32)).astype(np.int64)
+        return {"samples": lv[1:n + 1].tolist(), "rays": int(lv[0]), "iters": int(n),
+                "bar": rel[:, :, 0].tolist(), "scan": rel[:, :, 1].tolist(), "phase": rel[:, :, 2].tolist()}
 
     def export_state(self):
         """Full device state as host arrays (tables, pool, owners, stamps, requests,
