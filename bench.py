@@ -304,6 +304,8 @@ def main():
             if verbose:
                 print(f"timed {f}: {ms:.3f} ms samples {rec.samples} miss {rec.true_misses} "
                       f"it {sess.last_frame_stats.get('iterations')}", file=sys.stderr)
+            if os.environ.get("CINR_STATS"):
+                print("counters", f, sess.frame_counters(), file=sys.stderr)
             km, kn = sess.march_kernel_time()
             march_ms += km
             march_launches += kn

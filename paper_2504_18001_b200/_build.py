@@ -58,7 +58,8 @@ def build(force=False, verbose=False):
     logs = []
     for src, extra in SOURCES.items():
         obj = OUT_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", str(CSRC / src), "-o", str(obj)]
+        diag = ["-DCINR_STATS"] if os.environ.get("CINR_STATS") else []  # diagnostics build only
+        cmd = [nvcc(), *ARCH, *COMMON, *diag, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stderr)
         if r.returncode != 0:

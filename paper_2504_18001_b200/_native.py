@@ -110,6 +110,7 @@ _PROTOS = {
     "vcb_march_timing": (i32, [i32, vp, vp]),
     "vcb_last_launch_count": (i64, []),
     "vcb_frame_trace": (i32, [vp, i64, i32, i32, vp, vp]),
+    "vcb_frame_counters": (i32, [vp, i64, i32, vp]),
     "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
     "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
 }

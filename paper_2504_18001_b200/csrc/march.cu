@@ -389,6 +389,7 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
                        int nt);
 int64_t wave3_ws_bytes(int64_t npix, int max_it);
 int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned int* out, int* live);
+int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* out);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
@@ -487,6 +488,7 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 3) return launch_wave_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768);
+        if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
@@ -582,4 +584,10 @@ extern "C" int64_t vcb_last_launch_count(void) { return g_launches; }
 extern "C" int32_t vcb_frame_trace(const void* workspace, int64_t max_rays, int32_t max_iterations, int32_t n,
                                    uint32_t* stamps, int32_t* live) {
     return wave3_trace(workspace, max_rays, max_iterations, n, stamps, live);
+}
+
+// Diagnostics: the 7 u64 counters a CINR_STATS build of the default schedule keeps.
+extern "C" int32_t vcb_frame_counters(const void* workspace, int64_t max_rays, int32_t max_iterations,
+                                      int64_t* out7) {
+    return wave3_counters(workspace, max_rays, max_iterations, (long long*)out7);
 }

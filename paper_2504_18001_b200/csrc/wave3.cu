@@ -195,6 +195,13 @@ struct W3Ctx {
 // After the shade of a live sample: the advance of iteration k+1 (or the
 // iteration-cap flush) and the write of slot j of S_{k+1}.  Returns the
 // sampling flag of slot j.
+#ifdef CINR_STATS
+// diagnostics build: FrameCounters.pad as u64 [skip-loop steps, advances, max steps in one advance]
+#define W3_NSKIP , &nskip
+#else
+#define W3_NSKIP
+#endif
+
 __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w, const W3Ws& s, const W3Ctx& c,
                                        int nb, bool last, int id, long long j, double dx, double dy, double dz,
                                        double ten, double tex, long long cur, double cr, double cg, double cb,
@@ -204,7 +211,16 @@ __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w
     if (!last) {
         double cf = __longlong_as_double(cur);
         i64 ck = cur;
-        f = advance_one(c.ox, c.oy, c.oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, c.occ, c.mu_s);
+#ifdef CINR_STATS
+        int nskip = 0;
+#endif
+        f = advance_one(c.ox, c.oy, c.oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, c.occ, c.mu_s W3_NSKIP);
+#ifdef CINR_STATS
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(w.ctr->pad);
+        atomicAdd(st, (unsigned long long)nskip);
+        atomicAdd(st + 1, 1ull);
+        atomicMax(st + 2, (unsigned long long)nskip);
+#endif
         cur = p.adv.adaptive ? __double_as_longlong(cf) : (long long)ck;
     }
     if (f) {
@@ -242,8 +258,47 @@ __device__ __forceinline__ void w3_count_next(int* gnx, int* snx, long long jb, 
     }
 }
 
+// One queued true miss of iteration k-1 (sampler.py:276-279): field inference at the
+// sample, shade, then the advance of iteration k into the same slot of S_k.  Out of
+// line, so the register-hungry inference does not raise the phase's register budget.
+template <int kInr>
+static __device__ __noinline__ void w3_miss_item(const VcbFrameParams& p, const FrameWs& w, const W3Ws& s,
+                                                 const W3Ctx c, const MlpSmem mlp, const float* lut, bool smem_lut,
+                                                 long long q, int b, bool last, int* gnx, int* snx) {
+    const double hmax = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
+    const long long j = __ldcg(s.mlist + q);
+    const int id = __ldcg(s.id[b] + j);
+    const double tmid = __ldcg(s.tmid[b] + j), dt = __ldcg(s.dt[b] + j);
+    const long long cur = __ldcg(s.cur[b] + j);
+    double cr = __ldcg(s.cr[b] + j), cg = __ldcg(s.cg[b] + j), cb = __ldcg(s.cb[b] + j), tr = __ldcg(s.tr[b] + j);
+    const double dx = __ldg(w.ray_dir + 3 * id), dy = __ldg(w.ray_dir + 3 * id + 1), dz = __ldg(w.ray_dir + 3 * id + 2);
+    const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)), pz = DADD(c.oz, DMUL(dz, tmid));
+    int bad = 0;
+    const float v = field_eval<kInr>(p.field, clampd(px, 0.0, hmax), clampd(py, 0.0, hmax), clampd(pz, 0.0, hmax),
+                                     mlp, &bad);
+    if (bad) w.ctr->nonfinite = 1;
+    const bool dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr,
+                                                 cg, cb, tr)
+                               : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term,
+                                                  cr, cg, cb, tr);
+    int f = 0;
+    if (dead) {
+        w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
+        __stcg(s.id[b] + j, -1);
+    } else {
+        f = w3_next(p, w, s, c, b, last, id, j, dx, dy, dz, __ldg(w.ray_ten + id), __ldg(w.ray_tex + id), cur, cr,
+                    cg, cb, tr);
+    }
+    if (f) {
+        atomicAdd(gnx + (j >> 5), 1);
+        atomicAdd(snx + (j >> 10), 1);
+    }
+}
+
 template <int kInr, int NT>
-__global__ void __launch_bounds__(NT, 1) k_wave3_march(VcbFrameParams p, FrameWs w, W3Ws s, int max_it) {
+__global__ void __launch_bounds__(NT, 1)
+    k_wave3_march(const __grid_constant__ VcbFrameParams p, const __grid_constant__ FrameWs w,
+                  const __grid_constant__ W3Ws s, int max_it) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ W3Smem sm;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -338,39 +393,8 @@ __global__ void __launch_bounds__(NT, 1) k_wave3_march(VcbFrameParams p, FrameWs
                 int* gnx = s.gcnt + (k % 3) * s.maxg;
                 int* snx = s.scnt + (k % 3) * s.maxs;
                 const bool last = (k == max_it);
-                const double hmax = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
-                for (long long q = (long long)cta * NT + threadIdx.x; q < nm; q += (long long)G * NT) {
-                    const long long j = __ldcg(s.mlist + q);
-                    const int id = __ldcg(s.id[b] + j);
-                    const double tmid = __ldcg(s.tmid[b] + j), dt = __ldcg(s.dt[b] + j);
-                    const long long cur = __ldcg(s.cur[b] + j);
-                    double cr = __ldcg(s.cr[b] + j), cg = __ldcg(s.cg[b] + j), cb = __ldcg(s.cb[b] + j),
-                           tr = __ldcg(s.tr[b] + j);
-                    const double dx = __ldg(w.ray_dir + 3 * id), dy = __ldg(w.ray_dir + 3 * id + 1),
-                                 dz = __ldg(w.ray_dir + 3 * id + 2);
-                    const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)),
-                                 pz = DADD(c.oz, DMUL(dz, tmid));
-                    int bad = 0;
-                    const float v = field_eval<kInr>(p.field, clampd(px, 0.0, hmax), clampd(py, 0.0, hmax),
-                                                     clampd(pz, 0.0, hmax), mlp, &bad);
-                    if (bad) w.ctr->nonfinite = 1;
-                    const bool dead = s_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base,
-                                                              p.term, cr, cg, cb, tr)
-                                            : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive,
-                                                               p.adv.dt_base, p.term, cr, cg, cb, tr);
-                    int f = 0;
-                    if (dead) {
-                        w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
-                        __stcg(s.id[b] + j, -1);
-                    } else {
-                        f = w3_next(p, w, s, c, b, last, id, j, dx, dy, dz, __ldg(w.ray_ten + id),
-                                    __ldg(w.ray_tex + id), cur, cr, cg, cb, tr);
-                    }
-                    if (f) {
-                        atomicAdd(gnx + (j >> 5), 1);
-                        atomicAdd(snx + (j >> 10), 1);
-                    }
-                }
+                for (long long q = (long long)cta * NT + threadIdx.x; q < nm; q += (long long)G * NT)
+                    w3_miss_item<kInr>(p, w, s, c, mlp, lut, s_lut != nullptr, q, b, last, gnx, snx);
                 w3_barrier(s.bar, nbar++, G);
             }
         }
@@ -546,10 +570,10 @@ __global__ void __launch_bounds__(NT, 1) k_wave3_march(VcbFrameParams p, FrameWs
 }
 
 static const void* wave3_kernel(int mode, int nt) {
-    if (nt == 512)
-        return mode == 1 ? (const void*)k_wave3_march<1, 512>
-                         : mode == 2 ? (const void*)k_wave3_march<2, 512> : (const void*)k_wave3_march<0, 512>;
-    return mode == 1 ? (const void*)k_wave3_march<1, 768> : (const void*)k_wave3_march<0, 768>;
+    if (nt == 768) return mode == 1 ? (const void*)k_wave3_march<1, 768> : (const void*)k_wave3_march<0, 768>;
+    if (nt == 640) return mode == 1 ? (const void*)k_wave3_march<1, 640> : (const void*)k_wave3_march<0, 640>;
+    return mode == 1 ? (const void*)k_wave3_march<1, 512>
+                     : mode == 2 ? (const void*)k_wave3_march<2, 512> : (const void*)k_wave3_march<0, 512>;
 }
 
 void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
@@ -635,6 +659,15 @@ int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned
         cudaMemcpy(live, w.live, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
         return set_error("frame_trace: %s", cudaGetErrorString(cudaGetLastError()));
     return n;
+}
+
+int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* out) {
+    if (max_it > kMaxIterCap) max_it = kMaxIterCap;
+    FrameWs w;
+    frame_ws_layout(npix, max_it, const_cast<void*>(workspace), &w);
+    if (cudaMemcpy(out, w.ctr->pad, 7 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return set_error("frame_counters: %s", cudaGetErrorString(cudaGetLastError()));
+    return 0;
 }
 
 }  // namespace cinr

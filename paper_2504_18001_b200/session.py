@@ -292,6 +292,16 @@ class RenderSession:
         return {"samples": lv[1:n + 1].tolist(), "rays": int(lv[0]), "iters": int(n),
                 "bar": rel[:, :, 0].tolist(), "scan": rel[:, :, 1].tolist(), "phase": rel[:, :, 2].tolist()}
 
+    def frame_counters(self):
+        """The u64 diagnostics counters of the last frame (CINR_STATS builds)."""
+        self.stream.synchronize()
+        W = int(self.camera.width)
+        rows = self._band_rows(int(self.camera.height))
+        out = np.zeros(7, np.int64)
+        N.call("vcb_frame_counters", ptr(self._ws), W * rows, int(self.config.settings.max_iterations),
+               out.ctypes.data)
+        return out.tolist()
+
     def export_state(self):
         """Full device state as host arrays (tables, pool, owners, stamps, requests,
         staged loader batch): lets another implementation resume this session."""

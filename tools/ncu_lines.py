@@ -38,3 +38,34 @@ def main(rep, top=30):
 
 if __name__ == "__main__":
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+
+
+def by_ranges(rep, ranges):
+    """Sum instructions / stall samples over named (file, first, last) line ranges."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+                         capture_output=True, text=True).stdout
+    tot = {name: [0.0, 0.0] for name in ranges}
+    fname, hdr, ti, ts = "?", None, 0.0, 0.0
+    for r in csv.reader(out.splitlines()):
+        if r and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if not hdr or not r or not r[0]:
+            continue
+        try:
+            ins = float(r[hdr.index("Instructions Executed")])
+            st = float(r[hdr.index("Warp Stall Sampling (All Samples)")])
+            line = int(r[0])
+        except (ValueError, IndexError):
+            continue
+        ti += ins
+        ts += st
+        for name, (f, a, b) in ranges.items():
+            if fname == f and a <= line <= b:
+                tot[name][0] += ins
+                tot[name][1] += st
+    for name, (i, s) in tot.items():
+        print(f"{name:24s} {i / ti * 100:5.1f}% instr  {s / ts * 100:5.1f}% stall")
