@@ -237,9 +237,10 @@ int32_t vcb_march_timing(int32_t n_iters, double *ms_total, int64_t *launches);
  * Returns the number of iterations copied. */
 int32_t vcb_frame_trace(const void *workspace, int64_t max_rays, int32_t max_iterations, int32_t n,
                         uint32_t *stamps, int32_t *live);
-/* Diagnostics: 7 u64 counters of the last frame kept by a -DCINR_STATS build
- * (skip-loop steps, advances, max steps of one advance; zeros otherwise). */
-int32_t vcb_frame_counters(const void *workspace, int64_t max_rays, int32_t max_iterations, int64_t *out7);
+/* Diagnostics: 23 u64 counters of the last frame kept by a -DCINR_STATS build
+ * ([0..2] skip-loop steps, advances, max steps of one advance; [8..14] summed
+ * warp cycles per phase stage; zeros otherwise). */
+int32_t vcb_frame_counters(const void *workspace, int64_t max_rays, int32_t max_iterations, int64_t *out23);
 /* Kernels launched by this thread's last march_frame + maintenance calls. */
 int64_t vcb_last_launch_count(void);
 int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests);

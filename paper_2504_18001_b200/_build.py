@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
-SO = OUT_DIR / "libcinr_b200.so"
+SO = OUT_DIR / ("libcinr_b200_stats.so" if os.environ.get("CINR_STATS") else "libcinr_b200.so")
 INCLUDE = PKG.parent / "include"
 
 SOURCES = {
@@ -26,6 +26,7 @@ SOURCES = {
     "wave.cu": ["-fmad=false"],
     "wave2.cu": ["-fmad=false"],
     "wave3.cu": ["-fmad=false"],
+    "wave4.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
     "decode_tc.cu": [],
@@ -57,7 +58,7 @@ def build(force=False, verbose=False):
     objs = []
     logs = []
     for src, extra in SOURCES.items():
-        obj = OUT_DIR / (Path(src).stem + ".o")
+        obj = OUT_DIR / (Path(src).stem + (".stats.o" if os.environ.get("CINR_STATS") else ".o"))
         diag = ["-DCINR_STATS"] if os.environ.get("CINR_STATS") else []  # diagnostics build only
         cmd = [nvcc(), *ARCH, *COMMON, *diag, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)

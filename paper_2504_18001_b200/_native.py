@@ -7,6 +7,7 @@ raises NativeUnavailable.  Struct layouts mirror the header field for field.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import VoxcacheError
@@ -17,6 +18,8 @@ MAX_LAYERS = 8
 
 _LIB = None
 _SO = Path(__file__).resolve().parent / "_lib" / "libcinr_b200.so"
+if os.environ.get("CINR_STATS"):  # diagnostics build (tools only), built by `CINR_STATS=1 python -m ..._build`
+    _SO = _SO.with_name("libcinr_b200_stats.so")
 
 
 class NativeUnavailable(VoxcacheError):

@@ -388,12 +388,17 @@ int launch_wave2_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
 int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
                        int nt);
 int64_t wave3_ws_bytes(int64_t npix, int max_it);
+int64_t wave4_ws_bytes(int64_t npix, int max_it);
+int launch_wave4_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned int* out, int* live);
 int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* out);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
-    const int64_t a = wave3_ws_bytes(max_rays, max_iterations);  // includes frame_ws_layout
+    // the largest schedule layout (each includes frame_ws_layout)
+    int64_t a = wave3_ws_bytes(max_rays, max_iterations);
+    const int64_t a4 = wave4_ws_bytes(max_rays, max_iterations);
+    if (a4 > a) a = a4;
     const int64_t b = chain_ws_bytes(max_rays, max_iterations);
     return a > b ? a : b;
 }
@@ -489,6 +494,7 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768);
         if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640);
+        if (p.impl == 7) return launch_wave4_frame(p, st, &g_launches, ev, &g_ev_used);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
@@ -586,8 +592,8 @@ extern "C" int32_t vcb_frame_trace(const void* workspace, int64_t max_rays, int3
     return wave3_trace(workspace, max_rays, max_iterations, n, stamps, live);
 }
 
-// Diagnostics: the 7 u64 counters a CINR_STATS build of the default schedule keeps.
+// Diagnostics: the 23 u64 counters a CINR_STATS build of the default schedule keeps.
 extern "C" int32_t vcb_frame_counters(const void* workspace, int64_t max_rays, int32_t max_iterations,
-                                      int64_t* out7) {
-    return wave3_counters(workspace, max_rays, max_iterations, (long long*)out7);
+                                      int64_t* out23) {
+    return wave3_counters(workspace, max_rays, max_iterations, (long long*)out23);
 }

@@ -196,16 +196,27 @@ struct W3Ctx {
 // iteration-cap flush) and the write of slot j of S_{k+1}.  Returns the
 // sampling flag of slot j.
 #ifdef CINR_STATS
-// diagnostics build: FrameCounters.pad as u64 [skip-loop steps, advances, max steps in one advance]
+// diagnostics build: FrameCounters.pad as u64 [skip-loop steps, advances, max steps in one advance];
+// FrameWs.mq_pos as u64 [groups, cycles per phase stage 0..5] summed over warps
 #define W3_NSKIP , &nskip
+#define W3_T(q)                                                   \
+    do {                                                          \
+        __syncwarp(__activemask());                               \
+        const long long t_ = clock64();                           \
+        st_cyc[q] += t_ - t_prev;                                 \
+        t_prev = t_;                                              \
+    } while (0)
 #else
 #define W3_NSKIP
+#define W3_T(q) \
+    do {        \
+    } while (0)
 #endif
 
 __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w, const W3Ws& s, const W3Ctx& c,
                                        int nb, bool last, int id, long long j, double dx, double dy, double dz,
                                        double ten, double tex, long long cur, double cr, double cg, double cb,
-                                       double tr) {
+                                       double tr, int pix) {
     int f = 0;
     AdvanceOut a;
     if (!last) {
@@ -216,10 +227,26 @@ __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w
 #endif
         f = advance_one(c.ox, c.oy, c.oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, c.occ, c.mu_s W3_NSKIP);
 #ifdef CINR_STATS
-        unsigned long long* st = reinterpret_cast<unsigned long long*>(w.ctr->pad);
-        atomicAdd(st, (unsigned long long)nskip);
-        atomicAdd(st + 1, 1ull);
-        atomicMax(st + 2, (unsigned long long)nskip);
+        {
+            // warp-aggregated so the counters do not perturb the stage timings much
+            const unsigned am = __activemask();
+            int tot = nskip, mx = nskip;
+            for (int o = 16; o > 0; o >>= 1) {
+                const int ot = __shfl_xor_sync(am, tot, o), om = __shfl_xor_sync(am, mx, o);
+                if ((am >> ((threadIdx.x & 31) ^ o)) & 1u) {
+                    tot += ot;
+                    mx = max(mx, om);
+                }
+            }
+            if ((threadIdx.x & 31) == __ffs(am) - 1) {
+                unsigned long long* st = reinterpret_cast<unsigned long long*>(w.ctr->pad);
+                atomicAdd(st, (unsigned long long)tot);
+                atomicAdd(st + 1, (unsigned long long)__popc(am));
+                atomicMax(st + 2, (unsigned long long)mx);
+                atomicAdd(st + 3, (unsigned long long)mx);  // sum over warps of the slowest lane
+                atomicAdd(st + 4, 1ull);
+            }
+        }
 #endif
         cur = p.adv.adaptive ? __double_as_longlong(cf) : (long long)ck;
     }
@@ -233,7 +260,7 @@ __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w
         __stcg(s.cb[nb] + j, cb);
         __stcg(s.tr[nb] + j, tr);
     } else {
-        w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
+        w3_retire(p, pix, cr, cg, cb, tr);
         __stcg(s.id[nb] + j, -1);
     }
     return f;
@@ -287,7 +314,7 @@ static __device__ __noinline__ void w3_miss_item(const VcbFrameParams& p, const 
         __stcg(s.id[b] + j, -1);
     } else {
         f = w3_next(p, w, s, c, b, last, id, j, dx, dy, dz, __ldg(w.ray_ten + id), __ldg(w.ray_tex + id), cur, cr,
-                    cg, cb, tr);
+                    cg, cb, tr, __ldg(w.ray_pix + id));
     }
     if (f) {
         atomicAdd(gnx + (j >> 5), 1);
@@ -368,7 +395,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const long long cur0 = p.adv.adaptive ? __double_as_longlong(__ldg(w.ray_ten + id)) : 0ll;
                 f = w3_next(p, w, s, c, 0, max_it <= 0, id, i, __ldg(w.ray_dir + 3 * i), __ldg(w.ray_dir + 3 * i + 1),
                             __ldg(w.ray_dir + 3 * i + 2), __ldg(w.ray_ten + i), __ldg(w.ray_tex + i), cur0, 0.0,
-                            0.0, 0.0, 1.0);
+                            0.0, 0.0, 1.0, __ldg(w.ray_pix + i));
             }
             const int cnt = __popc(__ballot_sync(0xffffffffu, f));
             if (lane == 0) {
@@ -438,17 +465,32 @@ __global__ void __launch_bounds__(NT, 1)
             int* tick = s.tick + (k + 1);
             const long long nw = (long long)G * (NT / 32);
             long long g = (long long)cta * (NT / 32) + (threadIdx.x >> 5);
+            // slot ids and earlier-group counts of a group, loaded one group ahead
+            auto fetch = [&](long long gg, int& id_o, int& gc_o) {
+                const long long ii = gg * 32 + lane;
+                id_o = (gg < ng && ii < m) ? __ldcg(s.id[b] + ii) : -1;
+                const long long gg0 = gg & ~31ll;
+                gc_o = (gg < ng && gg0 + lane < gg) ? __ldcg(gcur + gg0 + lane) : 0;
+            };
+            int id_nx, gc_nx;
+            fetch(g, id_nx, gc_nx);
+#ifdef CINR_STATS
+            long long st_cyc[7] = {0, 0, 0, 0, 0, 0, 0};
+            long long t_prev = clock64();
+#endif
             while (g < ng) {
+                W3_T(6);
                 long long gnext = 0;
-                if (lane == 0) gnext = nw + atomicAdd(tick, 1);  // consumed at the end of the group
+                if (lane == 0) gnext = nw + atomicAdd(tick, 1);
                 const long long i = g * 32 + lane;
-                const int id = (i < m) ? __ldcg(s.id[b] + i) : -1;
+                const int id = id_nx;
                 // rank base: stripe prefix + earlier groups of the stripe
-                const long long g0 = g & ~31ll;
-                const int gc = (g0 + lane < g) ? __ldcg(gcur + g0 + lane) : 0;
-                const long long jb = (long long)s_sc[g >> 5] + warp_sum(gc);
+                const long long jb = (long long)s_sc[g >> 5] + warp_sum(gc_nx);
                 const unsigned bal = __ballot_sync(0xffffffffu, id >= 0);
                 const long long j = jb + __popc(bal & lt_mask);
+                const long long g_nx = __shfl_sync(0xffffffffu, gnext, 0);
+                fetch(g_nx, id_nx, gc_nx);
+                W3_T(0);
                 int f = 0, queued = 0;
                 if (id >= 0) {
                     const double tmid = __ldcg(s.tmid[b] + i), dt = __ldcg(s.dt[b] + i);
@@ -457,16 +499,24 @@ __global__ void __launch_bounds__(NT, 1)
                            tr = __ldcg(s.tr[b] + i);
                     const double dx = __ldg(w.ray_dir + 3 * id), dy = __ldg(w.ray_dir + 3 * id + 1),
                                  dz = __ldg(w.ray_dir + 3 * id + 2);
+                    const double ten = __ldg(w.ray_ten + id), tex = __ldg(w.ray_tex + id);
+                    const int pix = __ldg(w.ray_pix + id);
+                    const bool use_rng = p.cached && p.probe.mode != 2;
+                    const uint32_t r_prev = (use_rng && k > 0) ? __ldcg(w.rng + j) : 0u;
                     // the sample position as the advance computed it: o + d * tmid
                     const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)),
                                  pz = DADD(c.oz, DMUL(dz, tmid));
                     float v = 0.0f;
+#ifdef CINR_STATS
+                    if (px == -1234.5 || dt == -1.0 || cr == -1.0 || tr == -1.0) asm volatile("trap;");
+#endif
+                    W3_T(1);
                     if (!p.cached) {
                         queued = 1;
                     } else {
                         double u = 0.0;
-                        if (p.probe.mode != 2) {
-                            uint32_t r = (k == 0) ? lane_seed(p.rng_base, (u64)j) : __ldcg(w.rng + j);
+                        if (use_rng) {
+                            uint32_t r = (k == 0) ? lane_seed(p.rng_base, (u64)j) : r_prev;
                             r = xorshift32(r);
                             __stcg(w.rng + j, r);
                             u = DMUL((double)r, 2.3283064365386963e-10);  // / 2^32, exact
@@ -501,6 +551,10 @@ __global__ void __launch_bounds__(NT, 1)
                             c_fb += (sv != rq);
                         }
                     }
+#ifdef CINR_STATS
+                    if (v == -1234.5f) asm volatile("trap;");
+#endif
+                    W3_T(2);
                     if (queued) {
                         // the sample itself goes to slot j; the miss phase infers, shades, advances
                         c_ms += 1;
@@ -517,15 +571,16 @@ __global__ void __launch_bounds__(NT, 1)
                                                                   p.adv.dt_base, p.term, cr, cg, cb, tr)
                                                 : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive,
                                                                    p.adv.dt_base, p.term, cr, cg, cb, tr);
+                        W3_T(3);
                         if (dead) {
-                            w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
+                            w3_retire(p, pix, cr, cg, cb, tr);
                             __stcg(s.id[nb] + j, -1);
                         } else {
-                            f = w3_next(p, w, s, c, nb, last, id, j, dx, dy, dz, __ldg(w.ray_ten + id),
-                                        __ldg(w.ray_tex + id), cur, cr, cg, cb, tr);
+                            f = w3_next(p, w, s, c, nb, last, id, j, dx, dy, dz, ten, tex, cur, cr, cg, cb, tr, pix);
                         }
                     }
                 }
+                W3_T(4);
                 // queue this warp's true misses (one atomic per warp)
                 const unsigned qb = __ballot_sync(0xffffffffu, queued);
                 if (qb) {
@@ -535,8 +590,20 @@ __global__ void __launch_bounds__(NT, 1)
                     if (queued) __stcg(s.mlist + qbase + __popc(qb & lt_mask), (int)j);
                 }
                 w3_count_next(gnx, snx, jb, j, f);
-                g = __shfl_sync(0xffffffffu, gnext, 0);
+                g = g_nx;
+                W3_T(5);
+#ifdef CINR_STATS
+                st_cyc[6] -= 0;  // stage 6 = loop overhead + ticket (measured at the next top)
+#endif
             }
+#ifdef CINR_STATS
+            if (lane == 0) {
+                // light iterations (< 256 groups: one group per warp, pure latency) apart
+                unsigned long long* acc = reinterpret_cast<unsigned long long*>(w.mq_pos) + (ng < 256 ? 8 : 0);
+                for (int q = 0; q < 7; q++) atomicAdd(acc + 1 + q, (unsigned long long)st_cyc[q]);
+                if (st_cyc[0] != 0) atomicAdd(acc, 1ull);
+            }
+#endif
         }
         if (p.timing) {
             __syncthreads();
@@ -626,6 +693,9 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
         return set_error("march_frame: frame kernel does not fit one CTA per SM (%d B shared)", off);
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     cudaMemsetAsync(w.ctr_iter, 0, w.ctr_iter_bytes, st);
+#ifdef CINR_STATS
+    cudaMemsetAsync(w.mq_pos, 0, 16 * 8, st);
+#endif
     cudaMemsetAsync(s.gcnt, 0, (size_t)s.maxg * 3 * 4, st);
     cudaMemsetAsync(s.scnt, 0, (size_t)s.maxs * 3 * 4, st);
     cudaMemsetAsync(s.nmiss, 0, 8, st);
@@ -665,7 +735,8 @@ int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* o
     if (max_it > kMaxIterCap) max_it = kMaxIterCap;
     FrameWs w;
     frame_ws_layout(npix, max_it, const_cast<void*>(workspace), &w);
-    if (cudaMemcpy(out, w.ctr->pad, 7 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (cudaMemcpy(out, w.ctr->pad, 7 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(out + 7, w.mq_pos, 16 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
         return set_error("frame_counters: %s", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

@@ -297,7 +297,7 @@ class RenderSession:
         self.stream.synchronize()
         W = int(self.camera.width)
         rows = self._band_rows(int(self.camera.height))
-        out = np.zeros(7, np.int64)
+        out = np.zeros(23, np.int64)
         N.call("vcb_frame_counters", ptr(self._ws), W * rows, int(self.config.settings.max_iterations),
                out.ctypes.data)
         return out.tolist()

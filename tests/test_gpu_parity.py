@@ -211,7 +211,7 @@ def test_session_vs_oracle_random_scene(seed):
         scene_specs.SESSION_SPECS.pop(name, None)
 
 
-@pytest.mark.parametrize("other", [1, 2, 3, 4])
+@pytest.mark.parametrize("other", [1, 2, 3, 4, 7])
 def test_march_schedules_agree(other):
     """The persistent wavefront (default), the launch-per-iteration wavefront and
     the chained-CTA march are schedules of the same arithmetic: identical images
