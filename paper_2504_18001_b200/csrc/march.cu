@@ -386,7 +386,7 @@ int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
 int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 int launch_wave2_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
-                       int nt);
+                       int nt, int mu_mode);
 int64_t wave3_ws_bytes(int64_t npix, int max_it);
 int64_t wave4_ws_bytes(int64_t npix, int max_it);
 int launch_wave4_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
@@ -492,10 +492,11 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 3) return launch_wave_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
-        if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768);
-        if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640);
+        if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768, 0);
+        if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640, 0);
+        if (p.impl == 8) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 1);
         if (p.impl == 7) return launch_wave4_frame(p, st, &g_launches, ev, &g_ev_used);
-        return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512);
+        return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;

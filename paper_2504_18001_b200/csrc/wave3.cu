@@ -39,7 +39,34 @@
 namespace cinr {
 
 constexpr int kW3MaxStripeScan = 16384;     // stripes scanned in shared memory (16.7 M rays)
-constexpr long long kW3MuSmemCells = 40960;  // f32 majorants in smem up to 160 KB
+constexpr long long kW3MuSmemCells = 36864;  // f32 majorants in smem up to 144 KB
+
+// Per-warp shared-memory stage of the next group's slot state, filled by cp.async
+// one group ahead (512-thread CTAs: 16 x 3360 B).
+struct W3Stage {
+    double tmid[32], dt[32];
+    long long cur[32];
+    double cr[32], cg[32], cb[32], tr[32];
+    double dir[96];
+    double ten[32], tex[32];
+    int pix[32];
+    uint32_t rng[40];
+};
+
+__device__ __forceinline__ void w3_cp16(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void w3_cp8(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void w3_cp4(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void w3_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void w3_cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 constexpr long long kW3OccMaxCells = 1ll << 20;
 constexpr int kW3LutMax = 4096;
 constexpr int kW3TraceIters = 512;  // diagnostics: per-CTA timestamps of the first iterations
@@ -63,7 +90,7 @@ struct W3Ws {
     unsigned int* trace; // [kW3TraceIters][kW3TraceCtas][3] globaltimer low words (timing frames)
     long long maxg, maxs;
     // dynamic shared-memory carve (bytes)
-    int sm_lut, sm_mu, sm_occ, sm_mlp, sm_sc, sm_total;
+    int sm_lut, sm_mu, sm_occ, sm_mlp, sm_sc, sm_stage, sm_total;
 };
 
 inline int64_t w3_layout(int64_t n, int32_t max_it, void* base, W3Ws* s) {
@@ -75,13 +102,14 @@ inline int64_t w3_layout(int64_t n, int32_t max_it, void* base, W3Ws* s) {
     };
     const int64_t maxg = (n + 31) / 32 + 1;
     const int64_t maxs = (maxg + 31) / 32 + 1;
+    const int64_t ns = maxg * 32;  // whole groups, so 16-byte group copies stay in bounds
     size_t o_id[2], o_tm[2], o_dt[2], o_cur[2], o_c[2][4];
     for (int b = 0; b < 2; b++) {
-        o_id[b] = take((size_t)n * 4);
-        o_tm[b] = take((size_t)n * 8);
-        o_dt[b] = take((size_t)n * 8);
-        o_cur[b] = take((size_t)n * 8);
-        for (int q = 0; q < 4; q++) o_c[b][q] = take((size_t)n * 8);
+        o_id[b] = take((size_t)ns * 4);
+        o_tm[b] = take((size_t)ns * 8);
+        o_dt[b] = take((size_t)ns * 8);
+        o_cur[b] = take((size_t)ns * 8);
+        for (int q = 0; q < 4; q++) o_c[b][q] = take((size_t)ns * 8);
     }
     size_t o_g = take((size_t)maxg * 3 * 4);
     size_t o_s = take((size_t)maxs * 3 * 4);
@@ -224,8 +252,15 @@ __device__ __forceinline__ int w3_next(const VcbFrameParams& p, const FrameWs& w
         i64 ck = cur;
 #ifdef CINR_STATS
         int nskip = 0;
+        const long long ta0 = clock64();
 #endif
         f = advance_one(c.ox, c.oy, c.oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, c.occ, c.mu_s W3_NSKIP);
+#ifdef CINR_STATS
+        if (a.tmid == -1234.5) asm volatile("trap;");
+        const long long ta1 = clock64();
+        atomicAdd(reinterpret_cast<unsigned long long*>(w.ctr->pad) + 5, (unsigned long long)(ta1 - ta0));
+        atomicAdd(reinterpret_cast<unsigned long long*>(w.ctr->pad) + 6, 1ull);
+#endif
 #ifdef CINR_STATS
         {
             // warp-aggregated so the counters do not perturb the stage timings much
@@ -365,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0;
     __syncthreads();
 
-    unsigned long long c_ex = 0, c_fb = 0, c_ms = 0;
+    unsigned c_ex = 0, c_fb = 0, c_ms = 0;  // per-thread sample counts (< 2^32)
     long long req = 0;
 
     // diagnostics (timing frames): per CTA and iteration, globaltimer after the
@@ -474,6 +509,52 @@ __global__ void __launch_bounds__(NT, 1)
             };
             int id_nx, gc_nx;
             fetch(g, id_nx, gc_nx);
+            // cp.async staging of a group's state (512-thread CTAs): stage 1 = the slot
+            // arrays (16-byte L2 copies), stage 2 = ray data by id and the RNG lanes by rank
+            constexpr bool kStage = false;  // cp.async staging: measured slower (its smem evicts L1 pool lines)
+            W3Stage* stg = kStage ? reinterpret_cast<W3Stage*>(dsm + s.sm_stage) + (threadIdx.x >> 5) : nullptr;
+            const bool use_rng = p.cached && p.probe.mode != 2;
+            auto stage1 = [&](long long gg) {
+                if (gg >= ng) return;
+                const long long base = gg * 32;
+                for (int cix = lane; cix < 112; cix += 32) {
+                    const int a = cix >> 4, q = (cix & 15) * 2;
+                    const double* src;
+                    double* dst;
+                    switch (a) {
+                        case 0: src = s.tmid[b]; dst = stg->tmid; break;
+                        case 1: src = s.dt[b]; dst = stg->dt; break;
+                        case 2: src = reinterpret_cast<const double*>(s.cur[b]); dst = reinterpret_cast<double*>(stg->cur); break;
+                        case 3: src = s.cr[b]; dst = stg->cr; break;
+                        case 4: src = s.cg[b]; dst = stg->cg; break;
+                        case 5: src = s.cb[b]; dst = stg->cb; break;
+                        default: src = s.tr[b]; dst = stg->tr; break;
+                    }
+                    w3_cp16(dst + q, src + base + q);
+                }
+            };
+            auto stage2 = [&](long long gg, int idv, long long jbv, unsigned balv) {
+                if (gg >= ng) return;
+                if (idv >= 0) {
+                    w3_cp8(stg->dir + 3 * lane, w.ray_dir + 3 * (long long)idv);
+                    w3_cp8(stg->dir + 3 * lane + 1, w.ray_dir + 3 * (long long)idv + 1);
+                    w3_cp8(stg->dir + 3 * lane + 2, w.ray_dir + 3 * (long long)idv + 2);
+                    w3_cp8(stg->ten + lane, w.ray_ten + idv);
+                    w3_cp8(stg->tex + lane, w.ray_tex + idv);
+                    w3_cp4(stg->pix + lane, w.ray_pix + idv);
+                }
+                if (use_rng && k > 0 && balv) {
+                    const long long jal = jbv & ~3ll;
+                    const int nch = (int)((jbv + __popc(balv) - jal + 3) >> 2);
+                    if (lane < nch) w3_cp16(stg->rng + 4 * lane, w.rng + jal + 4 * lane);
+                }
+            };
+            if constexpr (kStage) {
+                stage1(g);
+                const long long jb0 = (g < ng ? (long long)s_sc[g >> 5] : 0) + warp_sum(gc_nx);
+                stage2(g, id_nx, jb0, __ballot_sync(0xffffffffu, id_nx >= 0));
+                w3_cp_commit();
+            }
 #ifdef CINR_STATS
             long long st_cyc[7] = {0, 0, 0, 0, 0, 0, 0};
             long long t_prev = clock64();
@@ -488,24 +569,62 @@ __global__ void __launch_bounds__(NT, 1)
                 const long long jb = (long long)s_sc[g >> 5] + warp_sum(gc_nx);
                 const unsigned bal = __ballot_sync(0xffffffffu, id >= 0);
                 const long long j = jb + __popc(bal & lt_mask);
+                // this group's state: from the stage (filled one group ahead) or from L2
+                double tmid = 0.0, dt = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, tr = 0.0;
+                double dx = 0.0, dy = 0.0, dz = 0.0, ten = 0.0, tex = 0.0;
+                long long cur = 0;
+                int pix = 0;
+                uint32_t r_prev = 0u;
+                if constexpr (kStage) {
+                    w3_cp_wait();
+                    __syncwarp();
+                    if (id >= 0) {
+                        tmid = stg->tmid[lane];
+                        dt = stg->dt[lane];
+                        cur = stg->cur[lane];
+                        cr = stg->cr[lane];
+                        cg = stg->cg[lane];
+                        cb = stg->cb[lane];
+                        tr = stg->tr[lane];
+                        dx = stg->dir[3 * lane];
+                        dy = stg->dir[3 * lane + 1];
+                        dz = stg->dir[3 * lane + 2];
+                        ten = stg->ten[lane];
+                        tex = stg->tex[lane];
+                        pix = stg->pix[lane];
+                        if (use_rng && k > 0) r_prev = stg->rng[j - (jb & ~3ll)];
+                    }
+                    __syncwarp();  // the stage is refilled below
+                } else if (id >= 0) {
+                    tmid = __ldcg(s.tmid[b] + i);
+                    dt = __ldcg(s.dt[b] + i);
+                    cur = __ldcg(s.cur[b] + i);
+                    cr = __ldcg(s.cr[b] + i);
+                    cg = __ldcg(s.cg[b] + i);
+                    cb = __ldcg(s.cb[b] + i);
+                    tr = __ldcg(s.tr[b] + i);
+                    dx = __ldg(w.ray_dir + 3 * id);
+                    dy = __ldg(w.ray_dir + 3 * id + 1);
+                    dz = __ldg(w.ray_dir + 3 * id + 2);
+                    ten = __ldg(w.ray_ten + id);
+                    tex = __ldg(w.ray_tex + id);
+                    pix = __ldg(w.ray_pix + id);
+                    if (use_rng && k > 0) r_prev = __ldcg(w.rng + j);
+                }
                 const long long g_nx = __shfl_sync(0xffffffffu, gnext, 0);
                 fetch(g_nx, id_nx, gc_nx);
+                if constexpr (kStage) stage1(g_nx);
+                // the sample position as the advance computed it: o + d * tmid
+                const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)),
+                             pz = DADD(c.oz, DMUL(dz, tmid));
+                if constexpr (kStage) {
+                    const long long jbn = (g_nx < ng ? (long long)s_sc[g_nx >> 5] : 0) + warp_sum(gc_nx);
+                    stage2(g_nx, id_nx, jbn, __ballot_sync(0xffffffffu, id_nx >= 0));
+                    w3_cp_commit();
+                }
                 W3_T(0);
                 int f = 0, queued = 0;
                 if (id >= 0) {
-                    const double tmid = __ldcg(s.tmid[b] + i), dt = __ldcg(s.dt[b] + i);
-                    const long long cur = __ldcg(s.cur[b] + i);
-                    double cr = __ldcg(s.cr[b] + i), cg = __ldcg(s.cg[b] + i), cb = __ldcg(s.cb[b] + i),
-                           tr = __ldcg(s.tr[b] + i);
-                    const double dx = __ldg(w.ray_dir + 3 * id), dy = __ldg(w.ray_dir + 3 * id + 1),
-                                 dz = __ldg(w.ray_dir + 3 * id + 2);
-                    const double ten = __ldg(w.ray_ten + id), tex = __ldg(w.ray_tex + id);
-                    const int pix = __ldg(w.ray_pix + id);
-                    const bool use_rng = p.cached && p.probe.mode != 2;
-                    const uint32_t r_prev = (use_rng && k > 0) ? __ldcg(w.rng + j) : 0u;
-                    // the sample position as the advance computed it: o + d * tmid
-                    const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)),
-                                 pz = DADD(c.oz, DMUL(dz, tmid));
                     float v = 0.0f;
 #ifdef CINR_STATS
                     if (px == -1234.5 || dt == -1.0 || cr == -1.0 || tr == -1.0) asm volatile("trap;");
@@ -613,13 +732,13 @@ __global__ void __launch_bounds__(NT, 1)
     }
 
     // ---- frame counters (FrameStats, mrpd.py:33-41)
-    c_ex = warp_sum(c_ex);
-    c_fb = warp_sum(c_fb);
-    c_ms = warp_sum(c_ms);
+    const unsigned long long t_ex = warp_sum((unsigned long long)c_ex);
+    const unsigned long long t_fb = warp_sum((unsigned long long)c_fb);
+    const unsigned long long t_ms = warp_sum((unsigned long long)c_ms);
     if (lane == 0) {
-        atomicAdd(&sm.cnt[0], c_ex);
-        atomicAdd(&sm.cnt[1], c_fb);
-        atomicAdd(&sm.cnt[2], c_ms);
+        atomicAdd(&sm.cnt[0], t_ex);
+        atomicAdd(&sm.cnt[1], t_fb);
+        atomicAdd(&sm.cnt[2], t_ms);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -647,7 +766,7 @@ void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
 
 // nt: threads per CTA (768 = 24 warps at <= 80 registers, 512 = 16 warps at <= 128)
 int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
-                       int nt) {
+                       int nt, int mu_mode) {
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
     FrameWs w;
@@ -667,11 +786,9 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
         off = o + bytes;
         return o;
     };
+    // fixed parts first, then the majorants in whatever shared memory is left
+    constexpr int kSmemMax = 227 * 1024;
     s.sm_lut = (p.lut_size <= kW3LutMax) ? take(p.lut_size * 16) : -1;
-    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
-    s.sm_mu = s.sm_occ = -1;
-    if (cells <= kW3MuSmemCells) s.sm_mu = take((int)cells * 4);
-    else if (cells <= kW3OccMaxCells && p.adv.skip_empty) s.sm_occ = take((int)(((cells + 31) >> 5) * 4));
     s.sm_mlp = -1;
     if (p.field.kind == 0) {
         int nw = 0, nb = 0;
@@ -684,6 +801,12 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
     if (s.maxs > kW3MaxStripeScan)
         return set_error("march_frame: %lld rays exceed the stripe scan budget", (long long)npix);
     s.sm_sc = take((int)s.maxs * 4);
+    s.sm_stage = -1;
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    s.sm_mu = s.sm_occ = -1;
+    if (mu_mode == 0 && cells <= kW3MuSmemCells && off + 16 + cells * 4 <= kSmemMax) s.sm_mu = take((int)cells * 4);
+    else if (cells <= kW3OccMaxCells && p.adv.skip_empty && off + 16 + ((cells + 31) >> 5) * 4 <= kSmemMax)
+        s.sm_occ = take((int)(((cells + 31) >> 5) * 4));
     s.sm_total = off;
     const void* fn = wave3_kernel(mode, nt);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
