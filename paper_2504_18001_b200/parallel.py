@@ -28,6 +28,14 @@ def init_from_env(backend=None) -> Ctx:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if ndev and local_world > ndev:
+        # more ranks than GPUs (a functional check of the multi-rank path on a small
+        # box): ranks share devices round-robin; NCCL cannot, so gloo carries the gather
+        local = local % ndev
+        backend = backend or "gloo"
+    backend = backend or os.environ.get("CINR_DIST_BACKEND") or None
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
