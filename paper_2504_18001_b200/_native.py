@@ -18,7 +18,9 @@ MAX_LAYERS = 8
 
 _LIB = None
 _SO = Path(__file__).resolve().parent / "_lib" / "libcinr_b200.so"
-if os.environ.get("CINR_STATS"):  # diagnostics build (tools only), built by `CINR_STATS=1 python -m ..._build`
+if os.environ.get("CINR_LIB"):  # tools: an alternative build of the same library (A/B measurements)
+    _SO = Path(os.environ["CINR_LIB"]).resolve()
+elif os.environ.get("CINR_STATS"):  # diagnostics build (tools only), built by `CINR_STATS=1 python -m ..._build`
     _SO = _SO.with_name("libcinr_b200_stats.so")
 
 
