@@ -154,14 +154,23 @@ __device__ __forceinline__ void w3_barrier(unsigned int* bar, int b, unsigned in
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned int* c = bar + b;
-        __threadfence();
-        atomicAdd(c, 1u);
+        // release: the CTA's writes (ordered before by bar.sync) become visible with the arrival
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
         unsigned int v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
         } while (v < G);
     }
     __syncthreads();
+}
+
+// Slot ids of group gg of S_k and the counts of the earlier groups of its stripe.
+__device__ __forceinline__ void w3_fetch(const W3Ws& s, int b, const int* gcur, long long m, long long ng,
+                                         long long gg, int lane, int& id_o, int& gc_o) {
+    const long long ii = gg * 32 + lane;
+    id_o = (gg < ng && ii < m) ? __ldcg(s.id[b] + ii) : -1;
+    const long long gg0 = gg & ~31ll;
+    gc_o = (gg < ng && gg0 + lane < gg) ? __ldcg(gcur + gg0 + lane) : 0;
 }
 
 // exclusive block scan of a[0..L) in place (shared memory); returns the total
@@ -447,9 +456,20 @@ __global__ void __launch_bounds__(NT, 1)
     for (;; k++) {
         w3_barrier(s.bar, nbar++, G);
         stamp(k, 0);
+        // one round of loads after the barrier: queued misses of k-1, the stripe counts
+        // and the first group of S_k (the last two again if a miss phase changes them)
+        const int nm = (k > 0) ? __ldcg(s.nmiss + (k - 1)) : 0;
+        const long long ng = (m + 31) >> 5;
+        const int ns = (int)((ng + 31) >> 5);
+        const int* gcur = s.gcnt + (k % 3) * s.maxg;
+        const long long g_first = (long long)cta * (NT / 32) + (threadIdx.x >> 5);
+        int id_nx = -1, gc_nx = 0;
+        if (k < max_it) {
+            for (int t = threadIdx.x; t < ns; t += NT) s_sc[t] = __ldcg(s.scnt + (k % 3) * s.maxs + t);
+            w3_fetch(s, k & 1, gcur, m, ng, g_first, lane, id_nx, gc_nx);
+        }
         if (k > 0) {
             // ---------------- miss phase of iteration k-1 (sampler.py:276-279)
-            const int nm = __ldcg(s.nmiss + (k - 1));
             if (nm > 0) {
                 const int b = k & 1;  // S_k
                 int* gnx = s.gcnt + (k % 3) * s.maxg;
@@ -458,6 +478,10 @@ __global__ void __launch_bounds__(NT, 1)
                 for (long long q = (long long)cta * NT + threadIdx.x; q < nm; q += (long long)G * NT)
                     w3_miss_item<kInr>(p, w, s, c, mlp, lut, s_lut != nullptr, q, b, last, gnx, snx);
                 w3_barrier(s.bar, nbar++, G);
+                if (k < max_it) {
+                    for (int t = threadIdx.x; t < ns; t += NT) s_sc[t] = __ldcg(s.scnt + (k % 3) * s.maxs + t);
+                    w3_fetch(s, k & 1, gcur, m, ng, g_first, lane, id_nx, gc_nx);
+                }
             }
         }
         if (k >= max_it) {
@@ -465,10 +489,6 @@ __global__ void __launch_bounds__(NT, 1)
             break;
         }
         // ---------------- scan of the stripe counts of S_k
-        const long long ng = (m + 31) >> 5;
-        const int ns = (int)((ng + 31) >> 5);
-        const int* gcur = s.gcnt + (k % 3) * s.maxg;
-        for (int t = threadIdx.x; t < ns; t += NT) s_sc[t] = __ldcg(s.scnt + (k % 3) * s.maxs + t);
         __syncthreads();
         const long long nk = w3_scan_array<NT>(s_sc, ns, sm.wsum);
         stamp(k, 1);
@@ -499,16 +519,9 @@ __global__ void __launch_bounds__(NT, 1)
             // the iteration has fewer groups than the grid has warps)
             int* tick = s.tick + (k + 1);
             const long long nw = (long long)G * (NT / 32);
-            long long g = (long long)cta * (NT / 32) + (threadIdx.x >> 5);
+            long long g = g_first;
             // slot ids and earlier-group counts of a group, loaded one group ahead
-            auto fetch = [&](long long gg, int& id_o, int& gc_o) {
-                const long long ii = gg * 32 + lane;
-                id_o = (gg < ng && ii < m) ? __ldcg(s.id[b] + ii) : -1;
-                const long long gg0 = gg & ~31ll;
-                gc_o = (gg < ng && gg0 + lane < gg) ? __ldcg(gcur + gg0 + lane) : 0;
-            };
-            int id_nx, gc_nx;
-            fetch(g, id_nx, gc_nx);
+            auto fetch = [&](long long gg, int& id_o, int& gc_o) { w3_fetch(s, b, gcur, m, ng, gg, lane, id_o, gc_o); };
             // cp.async staging of a group's state (512-thread CTAs): stage 1 = the slot
             // arrays (16-byte L2 copies), stage 2 = ray data by id and the RNG lanes by rank
             constexpr bool kStage = false;  // cp.async staging: measured slower (its smem evicts L1 pool lines)
