@@ -221,6 +221,8 @@ def main():
     ap.add_argument("--decode-n", type=int, default=1 << 24, help="isolated INR decode batch (0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="N>1: ranks write pixels straight into rank 0's frame (symmetric memory) instead of NCCL all-gather")
     ap.add_argument("--schedule", type=int, default=0,
                     help="march schedule (VcbFrameParams.impl): 0 one-barrier wavefront (default), 4 two-phase, 5 = 0 at 768 threads")
     args = ap.parse_args()
@@ -263,6 +265,18 @@ def main():
     sess.impl = args.schedule
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     st = sess.stream
+    fused = None
+    if args.fused_gather and ctx.world > 1 and ctx.backend == "nccl":
+        try:
+            fused = parallel.FusedGather(ctx, sess, args.res, args.res)
+        except Exception as exc:  # no peer mapping here: keep the NCCL all-gather
+            print(f"fused gather unavailable ({exc}); using NCCL all-gather", file=sys.stderr)
+            fused = None
+
+    def gather(img):
+        if fused is not None:
+            return fused.finish(st)
+        return parallel.gather_frame(ctx, img, st, args.res)
 
     def frame_device(f):
         sess.set_camera(traj.camera_at(f))
@@ -274,7 +288,7 @@ def main():
     verbose = bool(os.environ.get("CINR_BENCH_VERBOSE"))
     for f in range(args.warmup):
         img, t0 = frame_device(f)
-        parallel.gather_frame(ctx, img, st, args.res)
+        gather(img)
         rec = sess.collect_record(t0)
         if verbose:
             print(f"warm {f}: {rec.wall_s * 1e3:.2f} ms samples {rec.samples} miss {rec.true_misses} "
@@ -296,7 +310,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             img, t0 = frame_device(f)
-            parallel.gather_frame(ctx, img, st, args.res)
+            gather(img)
             e1.record(st)
             rec = sess.collect_record(t0)
             launches += N.load().vcb_last_launch_count()
@@ -335,7 +349,7 @@ def main():
                 img_h, rec = sess.render_frame()
             else:
                 img = sess.render_frame_device()
-                full = parallel.gather_frame(ctx, img, st, args.res)
+                full = gather(img)
                 img_h = full.cpu().numpy() if ctx.rank == 0 else None
                 rec = sess.collect_record(t0)
             walls.append(parallel.max_over_ranks(ctx, (time.perf_counter() - t0) * 1000.0))
@@ -380,7 +394,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 addressing + f32 samples",
             "data": "synthetic (random-init INR weights, procedural orbit)",
-            "config": {**workload(args.res, args.volume), "parallelism": f"sort-first bands x{ctx.world}",
+            "config": {**workload(args.res, args.volume),
+                       "parallelism": f"sort-first bands x{ctx.world}" + (", fused peer-write gather" if fused else ""),
                        "macro": msrc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(),

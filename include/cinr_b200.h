@@ -159,7 +159,9 @@ typedef struct {
     int32_t impl;            /* march schedule: 0 = one-barrier persistent wavefront (default), 1 = one launch
                                 per iteration, 2 = chained CTAs, 3 = persistent wavefront with look-back,
                                 4 = two-phase persistent wavefront, 5 = schedule 0 with 768 threads/CTA */
-    int32_t pad2_;
+    int32_t image_global;    /* 0: image is this session's band [rows][W][4]; 1: image is the whole
+                                frame [height][W][4] (possibly a peer GPU's buffer mapped over NVLink)
+                                and local row j lands on film row row0 + j*row_step */
 } VcbFrameParams;
 
 typedef struct {

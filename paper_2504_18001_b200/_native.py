@@ -84,7 +84,7 @@ class VcbFrameParams(C.Structure):
                 ("lut_size", i32), ("max_iterations", i32), ("epoch", C.c_uint32), ("timing", i32),
                 ("mu", vp), ("lut", vp), ("table", vp), ("pool", vp), ("last_used", vp), ("miss_count", vp),
                 ("field", VcbField), ("image", vp), ("stats", vp), ("workspace", vp), ("workspace_bytes", i64),
-                ("impl", i32), ("pad2_", i32)]
+                ("impl", i32), ("image_global", i32)]
 
 
 class VcbMaintParams(C.Structure):

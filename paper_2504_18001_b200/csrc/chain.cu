@@ -61,7 +61,7 @@ __device__ __forceinline__ void retire_px(const VcbFrameParams& p, int pix, doub
     o.y = __double2float_rn(DADD(cg, DMUL(tr, p.bg[1])));
     o.z = __double2float_rn(DADD(cb, DMUL(tr, p.bg[2])));
     o.w = __double2float_rn(DSUB(1.0, tr));
-    reinterpret_cast<float4*>(p.image)[pix] = o;
+    reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = o;
 }
 
 struct ChainSmem {
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kTile) k_chain_rays(VcbFrameParams p, FrameWs 
             film_coord((int)(i % W), p.cam.row0 + (int)(i / W) * p.cam.row_step, W, H, fx, fy);
             r = make_ray(fx, fy, p.cam);
             flag = r.keep;
-            reinterpret_cast<float4*>(p.image)[i] = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+            reinterpret_cast<float4*>(p.image)[frame_pixel(p, i)] = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
         }
         long long excl;
         const uint32_t total = ordered_scan(flag, tile, fw.status, tag, sm, excl);

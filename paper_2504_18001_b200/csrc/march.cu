@@ -127,7 +127,7 @@ __device__ __forceinline__ void retire(const VcbFrameParams& p, int pix, double 
     o.y = __double2float_rn(DADD(cg, DMUL(tr, p.bg[1])));
     o.z = __double2float_rn(DADD(cb, DMUL(tr, p.bg[2])));
     o.w = __double2float_rn(DSUB(1.0, tr));
-    reinterpret_cast<float4*>(p.image)[pix] = o;
+    reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = o;
 }
 
 // Pixel pass: background everywhere (raymarch.py:33-35), box hits flagged.
@@ -139,7 +139,7 @@ __global__ void k_raygen_frame(VcbFrameParams p, FrameWs w) {
         double fx, fy;
         film_coord((int)(i % W), p.cam.row0 + (int)(i / W) * p.cam.row_step, W, H, fx, fy);
         Ray r = make_ray(fx, fy, p.cam);
-        reinterpret_cast<float4*>(p.image)[i] = bg;
+        reinterpret_cast<float4*>(p.image)[frame_pixel(p, i)] = bg;
         w.pix_keep[i] = r.keep ? 1 : 0;
     }
 }

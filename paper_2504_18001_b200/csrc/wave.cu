@@ -36,7 +36,7 @@ __device__ __forceinline__ void retire_w(const VcbFrameParams& p, int pix, doubl
     o.y = __double2float_rn(DADD(cg, DMUL(tr, p.bg[1])));
     o.z = __double2float_rn(DADD(cb, DMUL(tr, p.bg[2])));
     o.w = __double2float_rn(DSUB(1.0, tr));
-    reinterpret_cast<float4*>(p.image)[pix] = o;
+    reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = o;
 }
 
 // sense-reversing grid barrier over the cooperative grid

@@ -39,7 +39,7 @@ __device__ __forceinline__ void w2_retire(const VcbFrameParams& p, int pix, doub
     o.y = __double2float_rn(DADD(cg, DMUL(tr, p.bg[1])));
     o.z = __double2float_rn(DADD(cb, DMUL(tr, p.bg[2])));
     o.w = __double2float_rn(DSUB(1.0, tr));
-    reinterpret_cast<float4*>(p.image)[pix] = o;
+    reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = o;
 }
 
 __device__ __forceinline__ void w2_barrier(unsigned int* count, volatile unsigned int* gen, unsigned int nblocks) {

@@ -88,6 +88,31 @@ def gather_frame(ctx: Ctx, img: torch.Tensor, stream=None, height=None) -> torch
         return gather_rows(ctx, img, height if height is not None else img.shape[0] * ctx.world)
 
 
+class FusedGather:
+    """Sort-first gather fused into the frame kernel: every rank's march kernel stores
+    its retired pixels straight into rank 0's frame buffer over NVLink (a symmetric-
+    memory peer mapping; VcbFrameParams.image_global), so the transfer overlaps the
+    march instead of following it.  One device-side barrier per frame orders the
+    peer stores before rank 0 reads the frame.  Opt-in (bench.py --fused-gather);
+    the NCCL all-gather stays the default."""
+
+    def __init__(self, ctx: Ctx, sess, height: int, width: int):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        dev = torch.device("cuda", ctx.local_rank)
+        self.ctx = ctx
+        self.local = symm_mem.empty((height, width, 4), dtype=torch.float32, device=dev)
+        self.hdl = symm_mem.rendezvous(self.local, dist.group.WORLD)
+        self.target = self.hdl.get_buffer(0, (height, width, 4), torch.float32)
+        sess.set_frame_target(self.target)
+
+    def finish(self, stream) -> torch.Tensor:
+        """Call after render_frame_device() on every rank; the full frame (rank 0)."""
+        with torch.cuda.stream(stream):
+            self.hdl.barrier(channel=0)
+        return self.local
+
+
 def barrier(ctx: Ctx):
     if ctx.world > 1:
         dist.barrier()

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+import weakref
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -106,12 +107,26 @@ class RenderSession:
         self.timing = False
         self.impl = 0  # march schedule (VcbFrameParams.impl): 0 = one-barrier persistent wavefront
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
+        self._target = None  # whole-frame buffer written in place (fused sort-first gather)
+        self._pin_free = []  # pinned host frames released by callers
 
     def set_band(self, row0: int, row_step: int):
         """Render only film rows row0 + j*row_step (one rank's share of a frame)."""
         if row_step < 1 or not 0 <= row0 < row_step:
             raise ValueError("band needs 0 <= row0 < row_step")
         self.band = (int(row0), int(row_step))
+
+    def set_frame_target(self, target):
+        """Write this session's rows straight into `target`, a whole-frame (H, W, 4) f32
+        CUDA tensor (e.g. rank 0's frame mapped over NVLink by symmetric memory), at
+        film rows row0 + j*row_step: the sort-first gather fused into the frame kernel.
+        None restores the session's own band image."""
+        if target is not None:
+            if target.dtype != torch.float32 or target.dim() != 3 or target.shape[2] != 4 or not target.is_cuda:
+                raise ValueError("frame target must be a CUDA f32 tensor of shape (H, W, 4)")
+            if not target.is_contiguous():
+                raise ValueError("frame target must be contiguous")
+        self._target = target
 
     def _band_rows(self, H: int) -> int:
         row0, step = self.band
@@ -203,6 +218,7 @@ class RenderSession:
         p.mu, p.lut = ptr(self._mu), ptr(self._lut)
         p.field = self._dfield.desc
         p.image = ptr(image)
+        p.image_global = 1 if (self._target is not None and image is self._target) else 0
         p.stats = ptr(self._stats)
         need = N.load().vcb_frame_workspace_bytes(W * p.cam.rows, p.max_iterations)
         if self._ws is None or self._ws.numel() < need:
@@ -216,9 +232,14 @@ class RenderSession:
         (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame."""
         W, H = int(self.camera.width), int(self.camera.height)
         R = self._band_rows(H)
-        if self._img is None or self._img.shape != (R, W, 4):
-            self._img = torch.empty((R, W, 4), dtype=torch.float32, device=self.device)
-        img = self._img
+        if self._target is not None:
+            if tuple(self._target.shape) != (H, W, 4):
+                raise ValueError(f"frame target shape {tuple(self._target.shape)} != {(H, W, 4)}")
+            img = self._target
+        else:
+            if self._img is None or self._img.shape != (R, W, 4):
+                self._img = torch.empty((R, W, 4), dtype=torch.float32, device=self.device)
+            img = self._img
         with torch.cuda.stream(self.stream):
             self._stats.zero_()
             p = self._frame_params(img)
@@ -259,11 +280,23 @@ class RenderSession:
         """Render, then run the maintenance phase; returns (image f32[H,W,4] on host, FrameRecord)."""
         t0 = time.perf_counter()
         img = self.render_frame_device()
-        host = torch.empty(img.shape, dtype=torch.float32, pin_memory=True)
+        host = self._pinned(tuple(img.shape))
         with torch.cuda.stream(self.stream):
             host.copy_(img, non_blocking=True)
         rec = self.collect_record(t0)
-        return host.numpy(), rec
+        out = host.numpy()
+        # the caller owns the array; its pinned buffer returns to the pool when it dies
+        weakref.finalize(out, self._pin_free.append, host)
+        return out, rec
+
+    def _pinned(self, shape):
+        """A pinned host frame buffer from the session's pool (pinned allocation costs
+        milliseconds, so buffers released by the caller are reused)."""
+        while self._pin_free:
+            t = self._pin_free.pop()
+            if tuple(t.shape) == shape:
+                return t
+        return torch.empty(shape, dtype=torch.float32, pin_memory=True)
 
     def march_kernel_time(self):
         """(ms, launches) of the ray-march kernel in the last timing=True frame."""

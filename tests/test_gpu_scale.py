@@ -165,8 +165,19 @@ def test_config5_sort_first_bands_join_bit_exact_4k():
         raise AssertionError("cache did not warm up")
 
     full = warm(make())
-    parts = [warm(make((r, 2))) for r in range(2)]
+    bands = [make((r, 2)) for r in range(2)]
+    parts = [warm(sb) for sb in bands]
     joined = np.empty_like(full)
     for r in range(2):
         joined[r::2] = parts[r]
     np.testing.assert_array_equal(joined, full)
+    # fused gather: each band session writes its rows straight into one shared frame
+    # buffer (what a peer GPU's symmetric-memory mapping looks like to the kernel)
+    import torch
+
+    frame = torch.full((H, W, 4), -1.0, dtype=torch.float32, device="cuda")
+    for sb in bands:
+        sb.set_frame_target(frame)
+        sb.render_frame()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(frame.cpu().numpy(), full)
