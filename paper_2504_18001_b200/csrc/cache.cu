@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
 template <int kInr>
 __global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* keys, const int64_t* n_keys_dev,
                                     int max_keys, float* out, int* nonfinite) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     MlpSmem m;
     const long long nk = *n_keys_dev;
     if (nk == 0) return;

@@ -96,7 +96,7 @@ __device__ __forceinline__ int block_scan(int flag, int* warp_tot, int& excl) {
 template <int kInr>
 __global__ void __launch_bounds__(kChainThreads, 2) k_chain_march(VcbFrameParams p, ChainWs w, const int* nrays, int G,
                                                                int max_it, unsigned int tag) {
-    extern __shared__ unsigned char dsmem[];
+    extern __shared__ __align__(16) unsigned char dsmem[];
     __shared__ ChainSmem sm;
     const int t = blockIdx.x;
     const long long M = *nrays;

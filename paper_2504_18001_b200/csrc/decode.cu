@@ -18,7 +18,7 @@ __device__ __forceinline__ long long brick_origin(long long idx, long long b, in
 template <int kInr>
 __global__ void k_field_bricks(VcbField F, VcbBrickGeom G, int64_t n_keys, const int64_t* __restrict__ keys,
                                float* __restrict__ out, int32_t* nonfinite) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     MlpSmem m;
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
@@ -54,7 +54,7 @@ __global__ void k_field_bricks(VcbField F, VcbBrickGeom G, int64_t n_keys, const
 template <int kInr>
 __global__ void k_field_points(VcbField F, int64_t n, const double* __restrict__ pos, float* __restrict__ out,
                                int32_t* nonfinite) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     MlpSmem m;
     if (F.kind == 0) {
         stage_mlp(F, smem, m);
@@ -73,7 +73,7 @@ __global__ void k_field_points(VcbField F, int64_t n, const double* __restrict__
 template <int kInr>
 __global__ void k_macro_minmax(VcbField F, long long vx, long long vy, long long vz, long long cell, long long gx,
                                long long gy, long long gz, float* vmin, float* vmax) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     __shared__ float rmin[32], rmax[32];
     MlpSmem m;
     if (F.kind == 0) {

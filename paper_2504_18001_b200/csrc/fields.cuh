@@ -78,11 +78,14 @@ __device__ __forceinline__ void encode_level(const VcbField& F, int l, double x,
 }
 
 // Default network (8 levels x 2 features -> 32 -> 32 -> 1): fully unrolled, registers.
+// The reference multiplies with OpenBLAS sgemm (fused multiply-adds, tolerance-only
+// parity, P14), so the products are explicit FMAs (immune to -fmad=false in the
+// march translation units) and weights come from shared memory four at a time.
 template <int IN, int H>
 __device__ __forceinline__ float mlp_2h(const float* feat, const MlpSmem& m, int out_sigmoid) {
-    const float* w0 = m.w;
-    const float* w1 = w0 + IN * H;
-    const float* w2 = w1 + H * H;
+    const float4* w0 = reinterpret_cast<const float4*>(m.w);
+    const float4* w1 = reinterpret_cast<const float4*>(m.w + IN * H);
+    const float* w2 = m.w + IN * H + H * H;
     const float* b0 = m.b;
     const float* b1 = b0 + H;
     const float* b2 = b1 + H;
@@ -91,8 +94,14 @@ __device__ __forceinline__ float mlp_2h(const float* feat, const MlpSmem& m, int
     for (int o = 0; o < H; o++) {
         float a = 0.0f;
 #pragma unroll
-        for (int k = 0; k < IN; k++) a += feat[k] * w0[o * IN + k];
-        a += b0[o];
+        for (int k = 0; k < IN / 4; k++) {
+            const float4 wv = w0[o * (IN / 4) + k];
+            a = __fmaf_rn(feat[4 * k], wv.x, a);
+            a = __fmaf_rn(feat[4 * k + 1], wv.y, a);
+            a = __fmaf_rn(feat[4 * k + 2], wv.z, a);
+            a = __fmaf_rn(feat[4 * k + 3], wv.w, a);
+        }
+        a = __fadd_rn(a, b0[o]);
         h0[o] = a > 0.0f ? a : 0.0f;
     }
     float h1[H];
@@ -100,14 +109,20 @@ __device__ __forceinline__ float mlp_2h(const float* feat, const MlpSmem& m, int
     for (int o = 0; o < H; o++) {
         float a = 0.0f;
 #pragma unroll
-        for (int k = 0; k < H; k++) a += h0[k] * w1[o * H + k];
-        a += b1[o];
+        for (int k = 0; k < H / 4; k++) {
+            const float4 wv = w1[o * (H / 4) + k];
+            a = __fmaf_rn(h0[4 * k], wv.x, a);
+            a = __fmaf_rn(h0[4 * k + 1], wv.y, a);
+            a = __fmaf_rn(h0[4 * k + 2], wv.z, a);
+            a = __fmaf_rn(h0[4 * k + 3], wv.w, a);
+        }
+        a = __fadd_rn(a, b1[o]);
         h1[o] = a > 0.0f ? a : 0.0f;
     }
     float zo = 0.0f;
 #pragma unroll
-    for (int k = 0; k < H; k++) zo += h1[k] * w2[k];
-    zo += b2[0];
+    for (int k = 0; k < H; k++) zo = __fmaf_rn(h1[k], w2[k], zo);
+    zo = __fadd_rn(zo, b2[0]);
     if (out_sigmoid) return 1.0f / (1.0f + expf(-zo));
     return zo < 0.0f ? 0.0f : (zo > 1.0f ? 1.0f : zo);
 }

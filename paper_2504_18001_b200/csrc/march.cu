@@ -314,7 +314,7 @@ void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st) {
 // clamp_normalized, 119-120), then shade the ray sitting at output slot j.
 template <int kInr>
 __global__ void k_miss_shade(VcbFrameParams p, FrameWs w, int k) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) float smem[];
     const int nm = __ldcg(&w.nmiss[k]);
     if (nm == 0) return;
     MlpSmem m;

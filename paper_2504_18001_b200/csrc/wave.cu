@@ -112,7 +112,7 @@ __device__ __forceinline__ long long round_scan(int flag, long long tile, int G,
 template <int kInr>
 __global__ void __launch_bounds__(kWaveThreads, 2) k_wave_march(VcbFrameParams p, FrameWs w, int max_it,
                                                                 unsigned int* bar) {
-    extern __shared__ unsigned char dsmem[];
+    extern __shared__ __align__(16) unsigned char dsmem[];
     __shared__ WaveSmem sm;
     MlpSmem mlp;
     int mlp_floats = 0;

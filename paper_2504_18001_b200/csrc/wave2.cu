@@ -86,7 +86,7 @@ __device__ __forceinline__ int w2_block_scan(int v, int* warp_tot, int& excl) {
 template <int kInr>
 __global__ void __launch_bounds__(kW2Threads, 2) k_wave2_march(VcbFrameParams p, FrameWs w, int max_it,
                                                                unsigned int* bar) {
-    extern __shared__ unsigned char dsmem[];
+    extern __shared__ __align__(16) unsigned char dsmem[];
     __shared__ W2Smem sm;
     MlpSmem mlp;
     int mlp_floats = 0;
