@@ -324,6 +324,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
     }
 }
 
+int inr_bricks_tc_dev(const VcbField& F, const VcbBrickGeom& G, const int64_t* keys, const int64_t* n_keys_dev,
+                      int max_keys, float* out, int32_t* nonfinite, cudaStream_t st);
+
 template <int kInr>
 __global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* keys, const int64_t* n_keys_dev,
                                     int max_keys, float* out, int* nonfinite) {
@@ -410,8 +413,13 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
     const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
     const int64_t* nst = (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged));
-    CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
-                      P.max_requests, P.staging, w.nonfinite);
+    if (P.field.kind == 0 && inr_is_default(P.field)) {
+        // the default INR decodes on the tensor cores (tcgen05, decode_tc.cu)
+        inr_bricks_tc_dev(P.field, P.geom, P.staged_keys, nst, P.max_requests, P.staging, w.nonfinite, st);
+    } else {
+        CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
+                          P.max_requests, P.staging, w.nonfinite);
+    }
     k_post_decode<<<1, 1, 0, st>>>(P, w);
     g_launches += 6;
     return check_launch("maintenance");

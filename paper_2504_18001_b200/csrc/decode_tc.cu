@@ -341,7 +341,11 @@ __device__ __forceinline__ void encode_level2(const VcbField& F, int l, const fl
 template <class Src>
 __global__ void __launch_bounds__(kTc2Threads, 1) k_inr_decode_tc2(const __grid_constant__ VcbField F, Src src,
                                                                    long long n, float* out, int32_t* nonfinite,
-                                                                   int n_smem_levels) {
+                                                                   int n_smem_levels, const int64_t* n_keys_dev,
+                                                                   long long per_key) {
+    // device-side item count (maintenance dispatches without a host round trip)
+    if (n_keys_dev != nullptr) n = *n_keys_dev * per_key;
+    if (n <= 0) return;
     extern __shared__ __align__(128) unsigned char dsm2[];
     Tc2Smem& sm = *reinterpret_cast<Tc2Smem*>(dsm2);
     float2* s_tab = reinterpret_cast<float2*>(dsm2 + ((sizeof(Tc2Smem) + 127) & ~size_t(127)));
@@ -476,7 +480,7 @@ static int tc2_smem_levels(const VcbField& F) {
 
 template <class Src>
 static int launch_tc2(const VcbField& F, const Src& src, long long n, float* out, int32_t* nonfinite,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int64_t* n_keys_dev = nullptr, long long per_key = 0) {
     const int L = tc2_smem_levels(F);
     const size_t smem = ((sizeof(Tc2Smem) + 127) & ~size_t(127)) + (size_t)(L > 0 ? F.tab_off[L] : 0) * 8;
     cudaFuncSetAttribute(k_inr_decode_tc2<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -484,7 +488,15 @@ static int launch_tc2(const VcbField& F, const Src& src, long long n, float* out
     long long grid = (tiles + kTc2Groups - 1) / kTc2Groups;
     if (grid > device_sms()) grid = device_sms();
     if (grid < 1) grid = 1;
-    k_inr_decode_tc2<Src><<<(int)grid, kTc2Threads, smem, st>>>(F, src, n, out, nonfinite, L);
+    k_inr_decode_tc2<Src><<<(int)grid, kTc2Threads, smem, st>>>(F, src, n, out, nonfinite, L, n_keys_dev, per_key);
+    return 0;
+}
+
+// Brick decode for maintenance: up to max_keys keys, count read on the device.
+int inr_bricks_tc_dev(const VcbField& F, const VcbBrickGeom& G, const int64_t* keys, const int64_t* n_keys_dev,
+                      int max_keys, float* out, int32_t* nonfinite, cudaStream_t st) {
+    const long long b3 = G.b * G.b * G.b;
+    launch_tc2(F, TcBricksSrc{G, keys}, (long long)max_keys * b3, out, nonfinite, st, n_keys_dev, b3);
     return 0;
 }
 
