@@ -305,6 +305,7 @@ def main():
 
     # ---- timed: device-resident frames, one CUDA event pair per frame on the session stream
     sess.timing = True
+    sess.trace = bool(os.environ.get("CINR_TRACE"))
     times, samples, march_ms, march_launches, launches, recs = [], 0, 0.0, 0, 0, []
     from paper_2504_18001_b200 import _native as N
 

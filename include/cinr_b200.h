@@ -144,7 +144,8 @@ typedef struct {
     int32_t lut_size;
     int32_t max_iterations;
     uint32_t epoch;          /* monotonic per call; tags look-back status words */
-    int32_t timing;          /* 1 = bracket every iteration kernel with CUDA events */
+    int32_t timing;          /* bit 0: bracket the frame kernel(s) with CUDA events; bit 1: record the
+                                default schedule's per-iteration trace (vcb_frame_trace) */
     const float *mu;         /* majorants [gz][gy][gx] */
     const float *lut;        /* [lut_size][4] */
     const int32_t *table;    /* dense logical MRPD, all LoDs */

@@ -414,7 +414,8 @@ __global__ void __launch_bounds__(NT, 1)
 
     // diagnostics (timing frames): per CTA and iteration, globaltimer after the
     // barrier, after the scan and when all of the CTA's warps finished the phase
-    const bool trace = p.timing && threadIdx.x == 0 && cta < kW3TraceCtas;
+    const bool tracing = (p.timing & 2) != 0;  // bit 1: per-iteration trace (diagnostics only)
+    const bool trace = tracing && threadIdx.x == 0 && cta < kW3TraceCtas;
     auto stamp = [&](int kk, int what) {
         if (trace && kk < kW3TraceIters) {
             unsigned long long t;
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(NT, 1)
         __syncthreads();
         const long long nk = w3_scan_array<NT>(s_sc, ns, sm.wsum);
         stamp(k, 1);
-        if (p.timing && cta == 0 && threadIdx.x == 0) w.live[k + 1] = (int)nk;
+        if (tracing && cta == 0 && threadIdx.x == 0) w.live[k + 1] = (int)nk;
         if (nk == 0) {
             iters = (n0 == 0) ? 0 : k + 1;
             break;
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
 #endif
         }
-        if (p.timing) {
+        if (tracing) {
             __syncthreads();
             stamp(k, 2);
         }

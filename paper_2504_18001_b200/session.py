@@ -104,7 +104,8 @@ class RenderSession:
         self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
-        self.timing = False
+        self.timing = False  # CUDA-event time the frame kernel (bench)
+        self.trace = False  # record the per-iteration trace (diagnostics)
         self.impl = 0  # march schedule (VcbFrameParams.impl): 0 = one-barrier persistent wavefront
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
         self._target = None  # whole-frame buffer written in place (fused sort-first gather)
@@ -213,7 +214,7 @@ class RenderSession:
         p.lut_size = self._lut.shape[0]
         p.max_iterations = int(s.max_iterations)
         p.epoch = _next_epoch()
-        p.timing = 1 if self.timing else 0
+        p.timing = (1 if self.timing else 0) | (2 if self.trace else 0)
         p.impl = self.impl
         p.mu, p.lut = ptr(self._mu), ptr(self._lut)
         p.field = self._dfield.desc

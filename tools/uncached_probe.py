@@ -20,6 +20,7 @@ sess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0),
 for f in range(3):
     sess.set_camera(traj.camera_at(10 + f)); sess.render_frame_device(); sess.collect_record(time.perf_counter())
 sess.timing = True
+sess.trace = True
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(sess.stream)
