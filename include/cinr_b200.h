@@ -227,6 +227,11 @@ int32_t vcb_inr_bricks_tc(const VcbField *f, const VcbBrickGeom *g, int64_t n_ke
 int32_t vcb_macro_minmax(const VcbField *f, const int64_t *dims, int64_t cell, float *vmin, float *vmax,
                          void *stream);
 
+/* macrocell.py:120-128 update_majorants on the device: mu[c] = f32(max of bin_max over
+ * bins [int(vmin[c]*bins), int(vmax[c]*bins)]), bin_max = opacity_bin_maxima (host, f64). */
+int32_t vcb_update_majorants(const float *vmin, const float *vmax, int64_t n, const double *bin_max, int32_t bins,
+                             float *mu, void *stream);
+
 /* ---- session ABI */
 int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);
 int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);

@@ -14,6 +14,7 @@ from .inr import HashGridConfig, InrField, InrModel, MLPConfig
 from .render import Camera, RenderSettings, TransferFunction, grayscale_ramp, transparent, warm_body
 from .sampler import LodPolicy, effective_lod_scale, force_max_scale
 from .scheduler import SchedulerConfig
+from .weights_io import load_weights, save_weights
 
 __version__ = "0.1.0"
 

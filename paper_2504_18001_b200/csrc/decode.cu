@@ -165,3 +165,44 @@ extern "C" int32_t vcb_macro_minmax(const VcbField* f, const int64_t* dims, int6
                       gy, gz, vmin, vmax);
     return check_launch("macro_minmax");
 }
+
+// macrocell.py:120-128 update_majorants: mu(cell) = max of the TF's binned opacity
+// maxima over bins [int(vmin*256), int(vmax*256)] (clamped), as f32.  The bins are
+// the reference's f64 opacity_bin_maxima (host, 256 values); a range max does not
+// depend on how the range is split, so this equals the reference's sparse-table
+// query bit for bit.  Runs on every TF change (16.8 M cells at 4096^3).
+namespace cinr {
+__global__ void k_update_majorants(const float* __restrict__ vmin, const float* __restrict__ vmax, int64_t n,
+                                   const double* __restrict__ bin_max, int bins, float* __restrict__ mu) {
+    __shared__ double tab[9][256];  // tab[k][i] = max over bins [i, i + 2^k)
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) tab[0][i] = bin_max[i];
+    __syncthreads();
+    int levels = 1;
+    for (int k = 1; (1 << k) <= bins && k < 9; k++) {
+        const int h = 1 << (k - 1);
+        for (int i = threadIdx.x; i + (1 << k) <= bins; i += blockDim.x) tab[k][i] = fmax(tab[k - 1][i], tab[k - 1][i + h]);
+        __syncthreads();
+        levels = k + 1;
+    }
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        // (value * bins) in f32 is exact for bins = 2^8; astype(int64) truncates
+        long long lo = (long long)(vmin[c] * (float)bins), hi = (long long)(vmax[c] * (float)bins);
+        lo = lo < 0 ? 0 : (lo > bins - 1 ? bins - 1 : lo);
+        hi = hi < 0 ? 0 : (hi > bins - 1 ? bins - 1 : hi);
+        if (hi < lo) hi = lo;
+        const int w = (int)(hi - lo + 1);
+        int k = 31 - __clz(w);
+        if (k > levels - 1) k = levels - 1;
+        mu[c] = (float)fmax(tab[k][lo], tab[k][hi - (1 << k) + 1]);
+    }
+}
+}  // namespace cinr
+
+extern "C" int32_t vcb_update_majorants(const float* vmin, const float* vmax, int64_t n, const double* bin_max,
+                                        int32_t bins, float* mu, void* stream) {
+    if (n <= 0) return 0;
+    if (bins < 1 || bins > 256) return cinr::set_error("update_majorants: bins must be in [1, 256]");
+    cinr::k_update_majorants<<<cinr::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(vmin, vmax, n, bin_max, bins,
+                                                                                         mu);
+    return cinr::check_launch("update_majorants");
+}

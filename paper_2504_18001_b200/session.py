@@ -135,8 +135,18 @@ class RenderSession:
 
     # -- control (session.py:78-101)
     def _set_majorants(self, tf):
-        macrocell.update_majorants(self.macro, tf)
-        self._mu = torch.from_numpy(np.ascontiguousarray(self.macro.majorant, dtype=np.float32)).to(self.device)
+        """macrocell.update_majorants on the device (vcb_update_majorants): the macro
+        grid's min/max stay resident; a TF change recomputes the majorants in place."""
+        m = self.macro
+        if getattr(self, "_vminmax", None) is None:
+            self._vminmax = (torch.from_numpy(np.ascontiguousarray(m.value_min, dtype=np.float32)).to(self.device),
+                             torch.from_numpy(np.ascontiguousarray(m.value_max, dtype=np.float32)).to(self.device))
+            self._mu = torch.empty(self._vminmax[0].shape, dtype=torch.float32, device=self.device)
+        bm = torch.from_numpy(macrocell.opacity_bin_maxima(tf)).to(self.device)
+        vmin, vmax = self._vminmax
+        N.call("vcb_update_majorants", ptr(vmin), ptr(vmax), vmin.numel(), ptr(bm), bm.numel(), ptr(self._mu),
+               stream_ptr(self.stream))
+        self._bm = bm  # keep alive until the stream ran
         self._lut = torch.from_numpy(np.ascontiguousarray(tf.lookup_table(), dtype=np.float32)).to(self.device)
 
     def set_camera(self, camera):

@@ -265,3 +265,34 @@ def test_tensor_core_decoder_vs_reference():
     geom = lay.geom()
     N.call("vcb_inr_bricks_tc", C.byref(df.desc), C.byref(geom), len(keys), ptr(kt), ptr(out), ptr(flag), 0)
     np.testing.assert_allclose(out.cpu().numpy().reshape(len(keys), -1), np.stack(refs), atol=1e-5, rtol=0)
+
+
+def test_update_majorants_on_device_matches_reference_rule():
+    """vcb_update_majorants (macrocell.py:120-128 on the device) equals the numpy
+    restatement (pinned to the reference by test_majorants_and_lut_vs_reference)
+    bit for bit, on random grids with values on bin edges and out of [0, 1]."""
+    import torch
+
+    import paper_2504_18001_b200 as P
+    from paper_2504_18001_b200 import _native as N
+    from paper_2504_18001_b200 import macrocell
+    from paper_2504_18001_b200.device import ptr
+
+    r = np.random.default_rng(11)
+    shape = (37, 41, 43)
+    a = r.random(shape).astype(np.float32)
+    b = r.random(shape).astype(np.float32)
+    vmin, vmax = np.minimum(a, b), np.maximum(a, b)
+    edges = r.random(shape) < 0.2
+    vmin[edges] = np.floor(vmin[edges] * 256) / 256
+    vmax[r.random(shape) < 0.05] = 1.25
+    vmin[r.random(shape) < 0.05] = -0.5
+    for tf in (P.warm_body(0.5, 0.9), P.grayscale_ramp(0.7), P.warm_body(0.35, 0.9)):
+        grid = macrocell.MacroCellGrid(16, (1, 1, 1), shape[::-1], vmin, vmax, np.ones(shape, np.float32))
+        want = macrocell.update_majorants(grid, tf).majorant
+        d_min, d_max = torch.from_numpy(vmin).cuda(), torch.from_numpy(vmax).cuda()
+        bm = torch.from_numpy(macrocell.opacity_bin_maxima(tf)).cuda()
+        mu = torch.empty_like(d_min)
+        N.call("vcb_update_majorants", ptr(d_min), ptr(d_max), d_min.numel(), ptr(bm), bm.numel(), ptr(mu), 0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(mu.cpu().numpy(), want)
