@@ -232,6 +232,10 @@ int32_t vcb_macro_minmax(const VcbField *f, const int64_t *dims, int64_t cell, f
 int32_t vcb_update_majorants(const float *vmin, const float *vmax, int64_t n, const double *bin_max, int32_t bins,
                              float *mu, void *stream);
 
+/* image_io.py:14-21 to_rgba8 on the device: out[i] = uint8(clip(f64(image[i]), 0, 1) * 255 + 0.5)
+ * for the n_pixels RGBA f32 pixels of image (frame streaming, protocol.py:59-61). */
+int32_t vcb_frame_rgba8(const float *image, int64_t n_pixels, uint8_t *out, void *stream);
+
 /* ---- session ABI */
 int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);
 int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);

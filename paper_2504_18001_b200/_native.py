@@ -111,6 +111,7 @@ _PROTOS = {
     "vcb_inr_bricks_tc": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
     "vcb_macro_minmax": (i32, [C.POINTER(VcbField), vp, i64, vp, vp, vp]),
     "vcb_update_majorants": (i32, [vp, vp, i64, vp, i32, vp, vp]),
+    "vcb_frame_rgba8": (i32, [vp, i64, vp, vp]),
     "vcb_frame_workspace_bytes": (i64, [i64, i32]),
     "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),
     "vcb_march_timing": (i32, [i32, vp, vp]),

@@ -206,3 +206,26 @@ extern "C" int32_t vcb_update_majorants(const float* vmin, const float* vmax, in
                                                                                          mu);
     return cinr::check_launch("update_majorants");
 }
+
+// image_io.py:14-21 to_rgba8: (clip(f64(x), 0, 1) * 255 + 0.5).astype(uint8), per channel,
+// on the device so a streamed frame leaves the GPU as 4 bytes per pixel.
+namespace cinr {
+__global__ void k_frame_rgba8(const float4* __restrict__ img, int64_t n, uchar4* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = img[i];
+        auto q = [](float x) -> unsigned char {
+            double d = (double)x;
+            d = d < 0.0 ? 0.0 : (d > 1.0 ? 1.0 : d);
+            return (unsigned char)(int)__dadd_rn(__dmul_rn(d, 255.0), 0.5);
+        };
+        out[i] = make_uchar4(q(v.x), q(v.y), q(v.z), q(v.w));
+    }
+}
+}  // namespace cinr
+
+extern "C" int32_t vcb_frame_rgba8(const float* image, int64_t n_pixels, uint8_t* out, void* stream) {
+    if (n_pixels <= 0) return 0;
+    cinr::k_frame_rgba8<<<cinr::grid_for(n_pixels, 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4*>(image), n_pixels, reinterpret_cast<uchar4*>(out));
+    return cinr::check_launch("frame_rgba8");
+}

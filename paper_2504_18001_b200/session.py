@@ -300,6 +300,21 @@ class RenderSession:
         weakref.finalize(out, self._pin_free.append, host)
         return out, rec
 
+    def render_frame_rgba8(self):
+        """render_frame() for streaming: the frame is quantised on the device exactly as
+        image_io.to_rgba8 (image_io.py:14-21) and 4 bytes per pixel cross PCIe.
+        Returns (uint8 (H, W, 4) host array, FrameRecord)."""
+        t0 = time.perf_counter()
+        img = self.render_frame_device()
+        if getattr(self, "_rgba8", None) is None or tuple(self._rgba8.shape) != tuple(img.shape):
+            self._rgba8 = torch.empty(tuple(img.shape), dtype=torch.uint8, device=self.device)
+        host = torch.empty(tuple(img.shape), dtype=torch.uint8, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            N.call("vcb_frame_rgba8", ptr(img), img.numel() // 4, ptr(self._rgba8), stream_ptr(self.stream))
+            host.copy_(self._rgba8, non_blocking=True)
+        rec = self.collect_record(t0)
+        return host.numpy(), rec
+
     def _pinned(self, shape):
         """A pinned host frame buffer from the session's pool (pinned allocation costs
         milliseconds, so buffers released by the caller are reused)."""
