@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "fields.cuh"
 #include "march.cuh"
+#include "mlp_warp.cuh"
 
 namespace cinr {
 
@@ -366,6 +367,58 @@ static __device__ __noinline__ void w3_miss_item(const VcbFrameParams& p, const 
     }
 }
 
+// The default INR's queued misses, 32 per warp: warp-cooperative inference with the
+// hidden layers on the tensor cores (mlp_warp.cuh), then per lane the same shade /
+// advance / publish as w3_miss_item.  Called converged by whole warps.
+static __device__ __noinline__ void w3_miss_warp(const VcbFrameParams& p, const FrameWs& w, const W3Ws& s,
+                                                 const W3Ctx c, const MlpFrag* fr, const float* lut, bool smem_lut,
+                                                 long long base, int nm, int b, bool last, int* gnx, int* snx) {
+    const double hmax = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
+    const long long q = base + (threadIdx.x & 31);
+    const bool active = q < nm;
+    long long j = 0, cur = 0;
+    int id = 0;
+    double tmid = 0.0, dt = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, tr = 1.0, dx = 0.0, dy = 0.0, dz = 0.0;
+    double px = 0.5, py = 0.5, pz = 0.5;
+    if (active) {
+        j = __ldcg(s.mlist + q);
+        id = __ldcg(s.id[b] + j);
+        tmid = __ldcg(s.tmid[b] + j);
+        dt = __ldcg(s.dt[b] + j);
+        cur = __ldcg(s.cur[b] + j);
+        cr = __ldcg(s.cr[b] + j);
+        cg = __ldcg(s.cg[b] + j);
+        cb = __ldcg(s.cb[b] + j);
+        tr = __ldcg(s.tr[b] + j);
+        dx = __ldg(w.ray_dir + 3 * id);
+        dy = __ldg(w.ray_dir + 3 * id + 1);
+        dz = __ldg(w.ray_dir + 3 * id + 2);
+        px = clampd(DADD(c.ox, DMUL(dx, tmid)), 0.0, hmax);
+        py = clampd(DADD(c.oy, DMUL(dy, tmid)), 0.0, hmax);
+        pz = clampd(DADD(c.oz, DMUL(dz, tmid)), 0.0, hmax);
+    }
+    float v = inr_warp_default(p.field, fr, px, py, pz);
+    if (!active) return;
+    if (!isfinite(v)) w.ctr->nonfinite = 1;
+    if (p.field.clip01) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+    const bool dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr,
+                                                 cg, cb, tr)
+                               : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term,
+                                                  cr, cg, cb, tr);
+    int f = 0;
+    if (dead) {
+        w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
+        __stcg(s.id[b] + j, -1);
+    } else {
+        f = w3_next(p, w, s, c, b, last, id, j, dx, dy, dz, __ldg(w.ray_ten + id), __ldg(w.ray_tex + id), cur, cr,
+                    cg, cb, tr, __ldg(w.ray_pix + id));
+    }
+    if (f) {
+        atomicAdd(gnx + (j >> 5), 1);
+        atomicAdd(snx + (j >> 10), 1);
+    }
+}
+
 template <int kInr, int NT>
 __global__ void __launch_bounds__(NT, 1)
     k_wave3_march(const __grid_constant__ VcbFrameParams p, const __grid_constant__ FrameWs w,
@@ -403,7 +456,14 @@ __global__ void __launch_bounds__(NT, 1)
     }
     MlpSmem mlp;
     mlp.w = mlp.b = nullptr;
-    if (kInr != 0 && s.sm_mlp >= 0) stage_mlp(p.field, reinterpret_cast<float*>(dsm + s.sm_mlp), mlp);
+    const MlpFrag* mfrag = nullptr;
+    if (kInr == 1 && s.sm_mlp >= 0) {
+        // default INR: B fragments for the tensor-core miss inference
+        stage_mlp_frag(p.field, reinterpret_cast<MlpFrag*>(dsm + s.sm_mlp));
+        mfrag = reinterpret_cast<const MlpFrag*>(dsm + s.sm_mlp);
+    } else if (kInr != 0 && s.sm_mlp >= 0) {
+        stage_mlp(p.field, reinterpret_cast<float*>(dsm + s.sm_mlp), mlp);
+    }
     int* s_sc = reinterpret_cast<int*>(dsm + s.sm_sc);
     const float* lut = s_lut ? s_lut : p.lut;
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0;
@@ -476,8 +536,14 @@ __global__ void __launch_bounds__(NT, 1)
                 int* gnx = s.gcnt + (k % 3) * s.maxg;
                 int* snx = s.scnt + (k % 3) * s.maxs;
                 const bool last = (k == max_it);
-                for (long long q = (long long)cta * NT + threadIdx.x; q < nm; q += (long long)G * NT)
-                    w3_miss_item<kInr>(p, w, s, c, mlp, lut, s_lut != nullptr, q, b, last, gnx, snx);
+                if (kInr == 1) {
+                    for (long long qb = ((long long)cta * (NT / 32) + (threadIdx.x >> 5)) * 32; qb < nm;
+                         qb += (long long)G * NT)
+                        w3_miss_warp(p, w, s, c, mfrag, lut, s_lut != nullptr, qb, nm, b, last, gnx, snx);
+                } else {
+                    for (long long q = (long long)cta * NT + threadIdx.x; q < nm; q += (long long)G * NT)
+                        w3_miss_item<kInr>(p, w, s, c, mlp, lut, s_lut != nullptr, q, b, last, gnx, snx);
+                }
                 w3_barrier(s.bar, nbar++, G);
                 if (k < max_it) {
                     for (int t = threadIdx.x; t < ns; t += NT) s_sc[t] = __ldcg(s.scnt + (k % 3) * s.maxs + t);
@@ -810,7 +876,7 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
             nw += p.field.widths[L] * p.field.widths[L + 1];
             nb += p.field.widths[L + 1];
         }
-        s.sm_mlp = take((nw + nb) * 4);
+        s.sm_mlp = take(mode == 1 ? (int)sizeof(MlpFrag) : (nw + nb) * 4);
     }
     if (s.maxs > kW3MaxStripeScan)
         return set_error("march_frame: %lld rays exceed the stripe scan budget", (long long)npix);
