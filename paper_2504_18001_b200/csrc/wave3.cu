@@ -42,32 +42,6 @@ namespace cinr {
 constexpr int kW3MaxStripeScan = 16384;     // stripes scanned in shared memory (16.7 M rays)
 constexpr long long kW3MuSmemCells = 36864;  // f32 majorants in smem up to 144 KB
 
-// Per-warp shared-memory stage of the next group's slot state, filled by cp.async
-// one group ahead (512-thread CTAs: 16 x 3360 B).
-struct W3Stage {
-    double tmid[32], dt[32];
-    long long cur[32];
-    double cr[32], cg[32], cb[32], tr[32];
-    double dir[96];
-    double ten[32], tex[32];
-    int pix[32];
-    uint32_t rng[40];
-};
-
-__device__ __forceinline__ void w3_cp16(void* dst, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void w3_cp8(void* dst, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void w3_cp4(void* dst, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void w3_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void w3_cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 constexpr long long kW3OccMaxCells = 1ll << 20;
 constexpr int kW3LutMax = 4096;
 constexpr int kW3TraceIters = 512;  // diagnostics: per-CTA timestamps of the first iterations
@@ -91,7 +65,7 @@ struct W3Ws {
     unsigned int* trace; // [kW3TraceIters][kW3TraceCtas][3] globaltimer low words (timing frames)
     long long maxg, maxs;
     // dynamic shared-memory carve (bytes)
-    int sm_lut, sm_mu, sm_occ, sm_mlp, sm_sc, sm_stage, sm_total;
+    int sm_lut, sm_mu, sm_occ, sm_mlp, sm_sc, sm_total;
 };
 
 inline int64_t w3_layout(int64_t n, int32_t max_it, void* base, W3Ws* s) {
@@ -589,52 +563,7 @@ __global__ void __launch_bounds__(NT, 1)
             long long g = g_first;
             // slot ids and earlier-group counts of a group, loaded one group ahead
             auto fetch = [&](long long gg, int& id_o, int& gc_o) { w3_fetch(s, b, gcur, m, ng, gg, lane, id_o, gc_o); };
-            // cp.async staging of a group's state (512-thread CTAs): stage 1 = the slot
-            // arrays (16-byte L2 copies), stage 2 = ray data by id and the RNG lanes by rank
-            constexpr bool kStage = false;  // cp.async staging: measured slower (its smem evicts L1 pool lines)
-            W3Stage* stg = kStage ? reinterpret_cast<W3Stage*>(dsm + s.sm_stage) + (threadIdx.x >> 5) : nullptr;
             const bool use_rng = p.cached && p.probe.mode != 2;
-            auto stage1 = [&](long long gg) {
-                if (gg >= ng) return;
-                const long long base = gg * 32;
-                for (int cix = lane; cix < 112; cix += 32) {
-                    const int a = cix >> 4, q = (cix & 15) * 2;
-                    const double* src;
-                    double* dst;
-                    switch (a) {
-                        case 0: src = s.tmid[b]; dst = stg->tmid; break;
-                        case 1: src = s.dt[b]; dst = stg->dt; break;
-                        case 2: src = reinterpret_cast<const double*>(s.cur[b]); dst = reinterpret_cast<double*>(stg->cur); break;
-                        case 3: src = s.cr[b]; dst = stg->cr; break;
-                        case 4: src = s.cg[b]; dst = stg->cg; break;
-                        case 5: src = s.cb[b]; dst = stg->cb; break;
-                        default: src = s.tr[b]; dst = stg->tr; break;
-                    }
-                    w3_cp16(dst + q, src + base + q);
-                }
-            };
-            auto stage2 = [&](long long gg, int idv, long long jbv, unsigned balv) {
-                if (gg >= ng) return;
-                if (idv >= 0) {
-                    w3_cp8(stg->dir + 3 * lane, w.ray_dir + 3 * (long long)idv);
-                    w3_cp8(stg->dir + 3 * lane + 1, w.ray_dir + 3 * (long long)idv + 1);
-                    w3_cp8(stg->dir + 3 * lane + 2, w.ray_dir + 3 * (long long)idv + 2);
-                    w3_cp8(stg->ten + lane, w.ray_ten + idv);
-                    w3_cp8(stg->tex + lane, w.ray_tex + idv);
-                    w3_cp4(stg->pix + lane, w.ray_pix + idv);
-                }
-                if (use_rng && k > 0 && balv) {
-                    const long long jal = jbv & ~3ll;
-                    const int nch = (int)((jbv + __popc(balv) - jal + 3) >> 2);
-                    if (lane < nch) w3_cp16(stg->rng + 4 * lane, w.rng + jal + 4 * lane);
-                }
-            };
-            if constexpr (kStage) {
-                stage1(g);
-                const long long jb0 = (g < ng ? (long long)s_sc[g >> 5] : 0) + warp_sum(gc_nx);
-                stage2(g, id_nx, jb0, __ballot_sync(0xffffffffu, id_nx >= 0));
-                w3_cp_commit();
-            }
 #ifdef CINR_STATS
             long long st_cyc[7] = {0, 0, 0, 0, 0, 0, 0};
             long long t_prev = clock64();
@@ -649,33 +578,13 @@ __global__ void __launch_bounds__(NT, 1)
                 const long long jb = (long long)s_sc[g >> 5] + warp_sum(gc_nx);
                 const unsigned bal = __ballot_sync(0xffffffffu, id >= 0);
                 const long long j = jb + __popc(bal & lt_mask);
-                // this group's state: from the stage (filled one group ahead) or from L2
+                // this group's state (SoA slots through L2; ray data through the read-only path)
                 double tmid = 0.0, dt = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, tr = 0.0;
                 double dx = 0.0, dy = 0.0, dz = 0.0, ten = 0.0, tex = 0.0;
                 long long cur = 0;
                 int pix = 0;
                 uint32_t r_prev = 0u;
-                if constexpr (kStage) {
-                    w3_cp_wait();
-                    __syncwarp();
-                    if (id >= 0) {
-                        tmid = stg->tmid[lane];
-                        dt = stg->dt[lane];
-                        cur = stg->cur[lane];
-                        cr = stg->cr[lane];
-                        cg = stg->cg[lane];
-                        cb = stg->cb[lane];
-                        tr = stg->tr[lane];
-                        dx = stg->dir[3 * lane];
-                        dy = stg->dir[3 * lane + 1];
-                        dz = stg->dir[3 * lane + 2];
-                        ten = stg->ten[lane];
-                        tex = stg->tex[lane];
-                        pix = stg->pix[lane];
-                        if (use_rng && k > 0) r_prev = stg->rng[j - (jb & ~3ll)];
-                    }
-                    __syncwarp();  // the stage is refilled below
-                } else if (id >= 0) {
+                if (id >= 0) {
                     tmid = __ldcg(s.tmid[b] + i);
                     dt = __ldcg(s.dt[b] + i);
                     cur = __ldcg(s.cur[b] + i);
@@ -693,15 +602,9 @@ __global__ void __launch_bounds__(NT, 1)
                 }
                 const long long g_nx = __shfl_sync(0xffffffffu, gnext, 0);
                 fetch(g_nx, id_nx, gc_nx);
-                if constexpr (kStage) stage1(g_nx);
                 // the sample position as the advance computed it: o + d * tmid
                 const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)),
                              pz = DADD(c.oz, DMUL(dz, tmid));
-                if constexpr (kStage) {
-                    const long long jbn = (g_nx < ng ? (long long)s_sc[g_nx >> 5] : 0) + warp_sum(gc_nx);
-                    stage2(g_nx, id_nx, jbn, __ballot_sync(0xffffffffu, id_nx >= 0));
-                    w3_cp_commit();
-                }
                 W3_T(0);
                 int f = 0, queued = 0;
                 if (id >= 0) {
@@ -881,7 +784,6 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
     if (s.maxs > kW3MaxStripeScan)
         return set_error("march_frame: %lld rays exceed the stripe scan budget", (long long)npix);
     s.sm_sc = take((int)s.maxs * 4);
-    s.sm_stage = -1;
     const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
     s.sm_mu = s.sm_occ = -1;
     if (mu_mode == 0 && cells <= kW3MuSmemCells && off + 16 + cells * 4 <= kSmemMax) s.sm_mu = take((int)cells * 4);

@@ -37,7 +37,7 @@
 namespace cinr {
 
 constexpr int kW4Threads = 512;
-constexpr int kW4Ring = 8;  // look-back words: levels k and k+8 share a row
+constexpr int kW4Ring = 64;  // look-back words: levels k and k+64 share a row (8 measurably aborted)
 constexpr long long kW4MuSmemCells = 40960;
 constexpr long long kW4OccMaxCells = 1ll << 20;
 constexpr int kW4LutMax = 4096;
