@@ -16,9 +16,11 @@ loader (deterministic), seed 0.  A step = one RenderSession.render_frame()
   cpu_baseline : the CPU oracle (restated reference, all host threads) rendering
           the same steady-state frame from the GPU session's exact cache state
 
-Multi-GPU (torchrun, N>1): sort-first horizontal bands, one private cache per GPU,
-band images all-gathered with NCCL every frame (scaling "strong": one full frame
-per step, split over N GPUs).
+Multi-GPU (torchrun, N>1): by default alternate-frame rendering — rank r renders
+the whole 1024^2 orbit frames r, r+N, ... with its own cache and the frames are
+all-gathered with NCCL each step (scaling "weak": N frames per step);
+`--mp tiles` renders sort-first row bands of every frame instead (scaling
+"strong"; limited by the ~190 dependent iterations per frame).
 
 `--impl reference` times the CPU oracle port alone (the reference path has no GPU
 code) on a bounded sample of the same workload; see the JSON `cpu_baseline.sample`.
@@ -222,6 +224,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--uncached-steps", type=int, default=5, help="frames of the no-cache INR baseline (0 = skip)")
+    ap.add_argument("--mp", default="auto", choices=["auto", "frames", "tiles"],
+                    help="N>1: 'frames' = alternate-frame rendering (each GPU renders whole 1024^2 frames of the orbit "
+                         "with its own cache, frames gathered over NCCL; weak scaling, the default), 'tiles' = sort-first "
+                         "row bands of every frame (strong scaling)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="N>1: ranks write pixels straight into rank 0's frame (symmetric memory) instead of NCCL all-gather")
     ap.add_argument("--schedule", type=int, default=0,
@@ -262,12 +268,21 @@ def main():
                         scheduler=P.SchedulerConfig(max_requests=40), policy=P.LodPolicy(1.2, 20),
                         settings=P.RenderSettings(), seed=0)
     traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=args.res, height=args.res)
-    sess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+    mp = ("frames" if ctx.world > 1 else "single") if args.mp == "auto" else args.mp
+    if ctx.world == 1:
+        mp = "single"
+    afr = mp == "frames"
+    sess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, bands=not afr)
     sess.impl = args.schedule
+    per_step = ctx.world if afr else 1  # 1024^2 frames completed per step, whole job
+
+    def cam(f):
+        # alternate-frame rendering: rank r renders orbit frames r, r + N, r + 2N, ...
+        return traj.camera_at(f * ctx.world + ctx.rank if afr else f)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     st = sess.stream
     fused = None
-    if args.fused_gather and ctx.world > 1 and ctx.backend == "nccl":
+    if args.fused_gather and ctx.world > 1 and ctx.backend == "nccl" and not afr:
         try:
             fused = parallel.FusedGather(ctx, sess, args.res, args.res)
         except Exception as exc:  # no peer mapping here: keep the NCCL all-gather
@@ -275,12 +290,14 @@ def main():
             fused = None
 
     def gather(img):
+        if afr:
+            return parallel.gather_frames(ctx, img, st)
         if fused is not None:
             return fused.finish(st)
         return parallel.gather_frame(ctx, img, st, args.res)
 
     def frame_device(f):
-        sess.set_camera(traj.camera_at(f))
+        sess.set_camera(cam(f))
         t0 = time.perf_counter()
         img = sess.render_frame_device()
         return img, t0
@@ -290,7 +307,7 @@ def main():
     for f in range(args.warmup):
         if ctx.world == 1 and f >= args.warmup - 2:
             # the last warm-up frames go through the public call too (pins its host frame buffers)
-            sess.set_camera(traj.camera_at(f))
+            sess.set_camera(cam(f))
             t0 = time.perf_counter()
             _, rec = sess.render_frame()
         else:
@@ -339,7 +356,7 @@ def main():
         Path(os.environ["CINR_TRACE"]).write_text(json.dumps(sess.frame_trace()))
     sess.timing = False
     total_ms = sum(times)
-    fps = args.steps / (total_ms / 1000.0)
+    fps = per_step * args.steps / (total_ms / 1000.0)
     samples_all = parallel.sum_over_ranks(ctx, samples)
 
     # ---- e2e through the public API (host image out), continuing the orbit
@@ -355,10 +372,10 @@ def main():
             flush.zero_()
             torch.cuda.synchronize()
             parallel.barrier(ctx)
-            sess.set_camera(traj.camera_at(f))
+            sess.set_camera(cam(f))
             t0 = time.perf_counter()
-            if ctx.world == 1:
-                img_h, rec = sess.render_frame()
+            if ctx.world == 1 or afr:
+                img_h, rec = sess.render_frame()  # AFR: every rank returns its whole frame to its host
             else:
                 img = sess.render_frame_device()
                 full = gather(img)
@@ -369,7 +386,7 @@ def main():
         if verbose:
             print("e2e walls ms:", [round(x, 2) for x in walls], file=sys.stderr)
         h2d = len(bytes(N.VcbFrameParams())) + len(bytes(N.VcbMaintParams()))
-        e2e = {"value": args.steps / (sum(walls) / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": per_step * args.steps / (sum(walls) / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "median_ms": statistics.median(walls), "max_ms": max(walls),
                "d2h_bytes_per_step": args.res * args.res * 16 + 256,
                "note": "RenderSession.render_frame(): camera/params by value, image f32[H,W,4] copied to host"}
@@ -439,10 +456,11 @@ def main():
         line = {
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64 addressing + f32 samples",
+            "scaling": "weak" if afr else "strong", "vs_baseline": None, "dtype": "f64 addressing + f32 samples",
             "data": "synthetic (random-init INR weights, procedural orbit)",
             "config": {**workload(args.res, args.volume),
-                       "parallelism": f"sort-first bands x{ctx.world}" + (", fused peer-write gather" if fused else ""),
+                       "parallelism": (f"alternate-frame rendering x{ctx.world} (private cache per GPU, NCCL frame gather)"
+                                       if afr else f"sort-first bands x{ctx.world}" + (", fused peer-write gather" if fused else "")),
                        "macro": msrc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(),
@@ -453,7 +471,7 @@ def main():
                          "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "inr_decode": decode, "uncached_inr_baseline": uncached,
             "clocks": clk.summary(), "gpu_launches": launches,
-            "samples_per_frame": samples_all / args.steps,
+            "samples_per_frame": samples_all / (args.steps * per_step),
             "inr_samples_per_frame": float(np.mean([r.true_misses for r in recs])) + 40 * 16 ** 3,
             "hit_rate": 1.0 - sum(r.true_misses for r in recs) / max(1, sum(r.samples for r in recs)),
             "last_record": {k: getattr(last, k) for k in ("frame", "samples", "true_misses", "fallback_hits",

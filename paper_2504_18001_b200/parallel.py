@@ -53,12 +53,30 @@ def rows_of(rank: int, world: int, height: int):
     return list(range(rank, height, world))
 
 
-def make_session(ctx: Ctx, field_src, tf, camera, config, macro=None):
+def make_session(ctx: Ctx, field_src, tf, camera, config, macro=None, bands: bool = True):
+    """A session on this rank's GPU: a sort-first band of every frame (bands=True) or
+    whole frames (alternate-frame rendering, bands=False)."""
     from .session import RenderSession
 
     s = RenderSession(field_src, tf, camera, config, macro=macro, device=torch.device("cuda", ctx.local_rank))
-    s.set_band(ctx.rank, ctx.world)
+    if bands:
+        s.set_band(ctx.rank, ctx.world)
     return s
+
+
+def gather_frames(ctx: Ctx, img: torch.Tensor, stream=None) -> torch.Tensor:
+    """Alternate-frame rendering: every rank's whole frame of this step, stacked
+    (world, H, W, 4), all-gathered with NCCL on the render stream."""
+    if ctx.world == 1:
+        return img.unsqueeze(0)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        out = torch.empty((ctx.world,) + tuple(img.shape), dtype=img.dtype, device=img.device)
+        if ctx.backend == "nccl":
+            dist.all_gather_into_tensor(out, img.contiguous())
+        else:
+            dist.all_gather(list(out.unbind(0)), img.contiguous())
+        return out
 
 
 def gather_rows(ctx: Ctx, band: torch.Tensor, height: int) -> torch.Tensor:
