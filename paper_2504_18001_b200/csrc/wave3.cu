@@ -14,8 +14,9 @@
 //   barrier     the only grid-wide sync of an iteration (one counter per
 //               barrier instance, no reset).
 //   scan        every CTA scans the m_k/1024 stripe counts in shared memory.
-//   phase k     warps take groups from a global ticket (dynamic balance across
-//               the whole GPU); a group's rank base = stripe prefix + the warp's
+//   phase k     warps take groups (first by warp id, then from a global ticket:
+//               dynamic balance across the whole GPU; the next group's slot ids
+//               are prefetched); a group's rank base = stripe prefix + the warp's
 //               own scan of the earlier group counts of that stripe; then per
 //               lane: stochastic LoD + MRPD probe + trilinear + stamp + miss
 //               filing (kernels.py:166-273, sampler.py:236-275); shade
@@ -25,10 +26,15 @@
 //   misses      true misses (sampler.py:276-279) are queued instead of being
 //               inferred inline; after the barrier, an iteration that queued any
 //               runs one dense miss phase (inference, shade, advance, count)
-//               and one more barrier.  Steady-state frames have none.
+//               and one more barrier.  Steady-state frames have none.  For the
+//               default INR the phase infers 32 misses per warp with the hidden
+//               layers on the tensor cores (mlp_warp.cuh).
 //
-// The majorant grid, the transfer-function LUT and the MLP weights live in
-// shared memory; per-sample state is SoA so every warp access is coalesced.
+// The majorant grid, the transfer-function LUT and the MLP weights (as mma
+// B fragments for the default INR) live in shared memory; per-sample state is
+// SoA so every warp access is coalesced.  Bit-exactness: all addressing, cursor,
+// LoD and compositing arithmetic is the reference's f64/f32 sequence without FMA
+// contraction (common.cuh); only inferred INR values are tolerance-level (P14).
 #include <cstddef>
 #include <cstdio>
 
