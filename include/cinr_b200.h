@@ -25,6 +25,8 @@
  *   Session ABI (Stage B drop-in: the GPU-resident RenderSession):
  *     vcb_march_frame   <- render/raymarch.py:25-120 raymarch_frame with the
  *                          VolumeSampler probe/miss path (sampler.py:196-280)
+ *     vcb_pathtrace_frame <- render/pathtrace.py:112-146 pathtrace_frame (trace_free_flight
+ *                          28-98, _light_visibility 101-109) on the same sampler
  *     vcb_maintenance   <- session.py:132-142 _maintenance: Mrpd.drain_miss_reports
  *                          (mrpd.py:263), RequestTable.report_many/select_batch
  *                          (scheduler.py:60-101), InlineLoader collect/dispatch
@@ -189,6 +191,26 @@ typedef struct {
     VcbField field;
 } VcbMaintParams;
 
+/* Path tracing (render/pathtrace.py:112-146, session.py:108-109): samples_per_pixel
+ * delta-tracked paths per pixel with one shadow ray each, on the VolumeSampler of the
+ * frame params (cache probe, miss filing, true-miss inference).  The PCG64 stream is
+ * numpy's default_rng(splitmix64((seed & 0xFFFFFFFF) ^ frame)) seeded on the host. */
+typedef struct {
+    int32_t spp;             /* SessionConfig.samples_per_pixel */
+    int32_t max_walk;        /* _MAX_WALK (pathtrace.py:18) */
+    double density;          /* RenderSettings.pt_density */
+    double ambient;          /* RenderSettings.pt_ambient */
+    double light[3];         /* -light_dir / |light_dir| (pathtrace.py:103-104) */
+    int32_t n_tf, pad_;
+    const double *tf;        /* [n_tf][5] TransferFunction.points (x, r, g, b, a), device */
+    uint64_t pcg_state[2];   /* PCG64 state (lo, hi) after seeding */
+    uint64_t pcg_inc[2];     /* PCG64 increment (lo, hi) */
+    uint64_t lane_seed;      /* VolumeSampler.seed (lane reseeding, sampler.py:206-213) */
+    int64_t lane_frame;      /* VolumeSampler.frame */
+    void *workspace;         /* vcb_pt_workspace_bytes(width*rows) bytes */
+    int64_t workspace_bytes;
+} VcbPtParams;
+
 const char *vcb_last_error(void);
 int32_t vcb_abi_version(void);
 int32_t vcb_device_sm_count(void);
@@ -239,6 +261,10 @@ int32_t vcb_frame_rgba8(const float *image, int64_t n_pixels, uint8_t *out, void
 /* ---- session ABI */
 int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);
 int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);
+/* render/pathtrace.py:112-146 pathtrace_frame with the VolumeSampler probe/miss path;
+ * the maintenance that follows is vcb_maintenance as for the ray march. */
+int64_t vcb_pt_workspace_bytes(int64_t max_rays);
+int32_t vcb_pathtrace_frame(const VcbFrameParams *p, const VcbPtParams *q, void *stream);
 /* After the stream of a timing=1 frame has completed: summed device time (ms) and
  * count of the first `n_iters` iteration-kernel launches (the ray-march kernel). */
 int32_t vcb_march_timing(int32_t n_iters, double *ms_total, int64_t *launches);

@@ -27,6 +27,7 @@ SOURCES = {
     "wave2.cu": ["-fmad=false"],
     "wave3.cu": ["-fmad=false"],
     "wave4.cu": ["-fmad=false"],
+    "pt.cu": ["-fmad=false"],
     "decode.cu": [],
     "cache.cu": [],
     "decode_tc.cu": [],

@@ -95,6 +95,12 @@ class VcbMaintParams(C.Structure):
                 ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField)]
 
 
+class VcbPtParams(C.Structure):
+    _fields_ = [("spp", i32), ("max_walk", i32), ("density", f64), ("ambient", f64), ("light", f64 * 3),
+                ("n_tf", i32), ("pad_", i32), ("tf", vp), ("pcg_state", C.c_uint64 * 2), ("pcg_inc", C.c_uint64 * 2),
+                ("lane_seed", C.c_uint64), ("lane_frame", i64), ("workspace", vp), ("workspace_bytes", i64)]
+
+
 _PROTOS = {
     "vcb_last_error": (C.c_char_p, []),
     "vcb_abi_version": (i32, []),
@@ -114,6 +120,8 @@ _PROTOS = {
     "vcb_frame_rgba8": (i32, [vp, i64, vp, vp]),
     "vcb_frame_workspace_bytes": (i64, [i64, i32]),
     "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),
+    "vcb_pt_workspace_bytes": (i64, [i64]),
+    "vcb_pathtrace_frame": (i32, [C.POINTER(VcbFrameParams), C.POINTER(VcbPtParams), vp]),
     "vcb_march_timing": (i32, [i32, vp, vp]),
     "vcb_last_launch_count": (i64, []),
     "vcb_frame_trace": (i32, [vp, i64, i32, i32, vp, vp]),
@@ -157,7 +165,7 @@ def load():
 
 
 STRUCTS = (VcbCamera, VcbMarchStatic, VcbProbeStatic, VcbField, VcbBrickGeom, VcbFrameStats, VcbCacheState,
-           VcbFrameParams, VcbMaintParams)
+           VcbFrameParams, VcbMaintParams, VcbPtParams)
 
 
 def struct_sizes():

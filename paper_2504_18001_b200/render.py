@@ -152,3 +152,16 @@ def base_step(dims, settings) -> float:
     """scene.py:41-44."""
     vx, vy, vz = dims
     return settings.base_step_scale * float(np.linalg.norm([1.0 / vx, 1.0 / vy, 1.0 / vz]))
+
+
+# -- path tracing host scalars (render/pathtrace.py) -----------------------------
+PT_MAX_WALK = 100_000  # pathtrace.py:18 _MAX_WALK
+
+
+def pcg64_seeded_state(seed: int):
+    """(state, inc) of numpy's default_rng(seed) (PCG64 after SeedSequence), as the
+    path tracer's stream starts (pathtrace.py:117).  The device advances it."""
+    st = np.random.default_rng(int(seed)).bit_generator.state
+    if st["bit_generator"] != "PCG64":
+        raise RuntimeError(f"numpy default_rng is {st['bit_generator']}, expected PCG64")
+    return int(st["state"]["state"]), int(st["state"]["inc"])

@@ -27,8 +27,9 @@ from . import macrocell
 from .cache import CacheConfig, DeviceCache
 from .device import device_field, ptr, require_cuda, stream_ptr
 from .errors import ConfigError, ModelCorruptError, RenderError
-from .render import RenderSettings, base_step, camera_rays_setup
-from .sampler import MODES, LodPolicy, effective_lod_scale, force_max_scale, frame_rng_base, point_to_unit_box
+from .render import PT_MAX_WALK, RenderSettings, base_step, camera_rays_setup, pcg64_seeded_state
+from .sampler import (MASK64, MODES, LodPolicy, effective_lod_scale, force_max_scale, frame_rng_base,
+                      point_to_unit_box, splitmix64)
 from .scheduler import SchedulerConfig
 
 
@@ -75,8 +76,8 @@ class RenderSession:
     def __init__(self, field_src, tf, camera, config: SessionConfig, macro=None, device=None, debug=False,
                  stream=None):
         self.device = require_cuda(device)
-        if config.mode not in ("raymarch",):
-            raise ConfigError("only mode='raymarch' is implemented on the GPU path")
+        if config.mode not in ("raymarch", "pathtrace"):
+            raise ValueError(f"unknown mode {config.mode!r}")
         if config.loader not in ("inline", "thread"):
             raise ValueError(f"unknown loader kind {config.loader!r}")
         self.field = field_src
@@ -148,6 +149,8 @@ class RenderSession:
                stream_ptr(self.stream))
         self._bm = bm  # keep alive until the stream ran
         self._lut = torch.from_numpy(np.ascontiguousarray(tf.lookup_table(), dtype=np.float32)).to(self.device)
+        # control points for the path tracer's np.interp (tf.opacity / tf.eval, transfer.py:28-56)
+        self._tfp = torch.from_numpy(np.array(tf.points, dtype=np.float64)).to(self.device)
 
     def set_camera(self, camera):
         self.camera = camera
@@ -162,8 +165,6 @@ class RenderSession:
     def set_mode(self, mode: str):
         if mode not in ("raymarch", "pathtrace"):
             raise ValueError(f"unknown mode {mode!r}")
-        if mode != "raymarch":
-            raise ConfigError("pathtrace is out of scope for the GPU path")
         self.mode = mode
 
     def reset_cache(self):
@@ -238,6 +239,35 @@ class RenderSession:
         p.workspace_bytes = self._ws.numel()
         return p
 
+    def _pt_params(self, p):
+        """pathtrace_frame's scalars (pathtrace.py:112-117, 101-104): the numpy PCG64
+        stream of default_rng(splitmix64((seed & 0xFFFFFFFF) ^ frame)) as seeded state,
+        the normalised light direction, the TF control points."""
+        cfg = self.config
+        s = cfg.settings
+        q = N.VcbPtParams()
+        q.spp = int(cfg.samples_per_pixel)
+        q.max_walk = PT_MAX_WALK
+        q.density = float(s.pt_density)
+        q.ambient = float(s.pt_ambient)
+        light = -np.asarray(s.light_dir, dtype=np.float64)
+        light /= np.linalg.norm(light)
+        for a in range(3):
+            q.light[a] = float(light[a])
+        q.n_tf = int(self._tfp.shape[0])
+        q.tf = ptr(self._tfp)
+        st, inc = pcg64_seeded_state(splitmix64((cfg.seed & 0xFFFFFFFF) ^ self.frame))
+        q.pcg_state[0], q.pcg_state[1] = st & MASK64, st >> 64
+        q.pcg_inc[0], q.pcg_inc[1] = inc & MASK64, inc >> 64
+        q.lane_seed = cfg.seed & MASK64
+        q.lane_frame = self.frame
+        need = N.load().vcb_pt_workspace_bytes(int(p.cam.width) * int(p.cam.rows))
+        if getattr(self, "_pt_ws", None) is None or self._pt_ws.numel() < need:
+            self._pt_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        q.workspace = ptr(self._pt_ws)
+        q.workspace_bytes = self._pt_ws.numel()
+        return q
+
     def render_frame_device(self):
         """Render + maintenance on the session stream; returns the device image
         (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame."""
@@ -254,7 +284,11 @@ class RenderSession:
         with torch.cuda.stream(self.stream):
             self._stats.zero_()
             p = self._frame_params(img)
-            N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
+            if self.mode == "pathtrace":
+                q = self._pt_params(p)
+                N.call("vcb_pathtrace_frame", C.byref(p), C.byref(q), stream_ptr(self.stream))
+            else:
+                N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
             if self.cache is not None:
                 self.cache.maintenance(self.frame, self._dfield.desc, self.stream)
             # one small D2H for the FrameRecord counters

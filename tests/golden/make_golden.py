@@ -80,6 +80,8 @@ def make_tf(name):
 def session_config(spec):
     return SessionConfig(
         cached=spec.get("cached", True),
+        mode=spec.get("mode", "raymarch"),
+        samples_per_pixel=spec.get("spp", 1),
         loader="inline",
         cache=CacheConfig(
             brick_size=spec["brick"],
@@ -353,15 +355,17 @@ def save_rng():
     np.savez_compressed(HERE / "rng.npz", **out)
 
 
-def main():
-    save_brickmath()
-    save_rng()
-    save_fields()
-    save_inr()
+def main(only=()):
+    if not only:
+        save_brickmath()
+        save_rng()
+        save_fields()
+        save_inr()
     for name, spec in specs.SESSION_SPECS.items():
-        save_session(name, spec, op_frame=spec.get("op_frame"))
+        if not only or name in only:
+            save_session(name, spec, op_frame=spec.get("op_frame"))
 
 
 if __name__ == "__main__":
     assert "voxcache" in sys.modules and os.path.isdir("/root/reference")
-    main()
+    main(tuple(sys.argv[1:]))  # optional: only these session names

@@ -87,4 +87,28 @@ SESSION_SPECS = {
         brick=16, pool=(2, 2, 2), policy=dict(lod_scale=1.2, preload_frames=20),
         res=(48, 48), frames=2, cam_step=30,
     ),
+    # path tracing (pathtrace.py:112-146, §8f row 2): Woodcock delta tracking over the
+    # majorants with the numpy PCG64 stream, the same cached sampler, shadow rays
+    "pt_lattice64": dict(
+        field="lattice", field_seed=7, dims=(64, 64, 64), tf=("warm_body", 0.45, 0.9), mode="pathtrace", spp=2,
+        brick=16, pool=(4, 4, 4), policy=dict(lod_scale=1.2, preload_frames=3),
+        settings=dict(pt_density=25.0), res=(48, 48), frames=8, cam_step=5,
+    ),
+    "pt_pressure": dict(
+        field="lattice", field_seed=13, dims=(64, 64, 64), tf=("warm_body", 0.4, 0.9), mode="pathtrace", spp=1,
+        brick=8, pool=(3, 3, 2), sched_kw=dict(max_requests=7),
+        policy=dict(lod_scale=0.5, preload_frames=2, mode="as_printed"),
+        settings=dict(pt_density=60.0, background=(0.1, 0.2, 0.3), light_dir=(0.3, -1.0, 0.2)),
+        res=(40, 36), frames=8, cam_step=2, radius=1.7, seed=5,
+    ),
+    "pt_inr": dict(
+        field="inr", dims=(64, 64, 64), tf=("warm_body", 0.5, 0.9), mode="pathtrace", spp=1,
+        brick=16, pool=(4, 4, 4), policy=dict(lod_scale=1.2, preload_frames=20),
+        settings=dict(pt_density=40.0), res=(40, 40), frames=5, cam_step=10,
+    ),
+    "pt_inr_uncached": dict(
+        field="inr", dims=(32, 32, 32), tf=("warm_body", 0.5, 0.9), mode="pathtrace", spp=1, cached=False,
+        brick=16, pool=(2, 2, 2), policy=dict(lod_scale=1.2, preload_frames=20),
+        settings=dict(pt_density=40.0), res=(32, 32), frames=2, cam_step=30,
+    ),
 }

@@ -65,7 +65,8 @@ def test_operator_passes_bit_exact_vs_reference(name):
     assert n >= 1
 
 
-EXACT = ["lattice64", "lattice64_paged", "lattice64_fifo", "aniso_b10", "events", "pressure", "pressure_fifo"]
+EXACT = ["lattice64", "lattice64_paged", "lattice64_fifo", "aniso_b10", "events", "pressure", "pressure_fifo",
+         "pt_lattice64", "pt_pressure"]
 
 
 @pytest.mark.parametrize("name", EXACT)
@@ -89,7 +90,7 @@ def test_session_bit_exact_vs_reference(name):
         assert diff <= 1e-6, f"frame {f} image max abs diff {diff}"
 
 
-@pytest.mark.parametrize("name", ["inr64", "inr_uncached"])
+@pytest.mark.parametrize("name", ["inr64", "inr_uncached", "pt_inr", "pt_inr_uncached"])
 def test_session_inr_vs_reference(name):
     """Random-init hash-grid INR: images within 1e-3 abs (>= 60 dB), cache state bit-exact."""
     from gpu_runner import run_gpu_session
