@@ -265,6 +265,19 @@ int32_t vcb_march_frame(const VcbFrameParams *p, void *stream);
  * the maintenance that follows is vcb_maintenance as for the ray march. */
 int64_t vcb_pt_workspace_bytes(int64_t max_rays);
 int32_t vcb_pathtrace_frame(const VcbFrameParams *p, const VcbPtParams *q, void *stream);
+/* render/pathtrace.py:28-98 trace_free_flight(scene, origins, directions, t_start, t_end, rng)
+ * on n caller rays (device arrays; o/d [n][3]) with the sampler, macro grid and field of p and
+ * the density / TF / PCG stream of q (q.spp unused); q.workspace holds vcb_pt_workspace_bytes(n).
+ * Synchronous: on return t_hit (+inf = escaped), v_hit are written and *draws (host) is the
+ * number of PCG64 draws consumed (the caller advances its generator by it). */
+int32_t vcb_trace_free_flight(const VcbFrameParams *p, const VcbPtParams *q, int64_t n, const double *o,
+                              const double *d, const double *t0, const double *t1, double *t_hit, float *v_hit,
+                              uint64_t *draws, void *stream);
+/* diagnostics: log1p_out[i] = glibc log1p(x[i]); uniform_out[i] = numpy PCG64 random() of
+ * draw draw_idx[i] (0-based) of the stream at pcg = {state lo, state hi, inc lo, inc hi};
+ * pcg is a HOST pointer, the rest device pointers */
+int32_t vcb_debug_pt_math(int64_t n, const double *x, double *log1p_out, const uint64_t *pcg,
+                          const uint64_t *draw_idx, double *uniform_out, void *stream);
 /* After the stream of a timing=1 frame has completed: summed device time (ms) and
  * count of the first `n_iters` iteration-kernel launches (the ray-march kernel). */
 int32_t vcb_march_timing(int32_t n_iters, double *ms_total, int64_t *launches);

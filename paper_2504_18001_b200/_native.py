@@ -122,6 +122,9 @@ _PROTOS = {
     "vcb_march_frame": (i32, [C.POINTER(VcbFrameParams), vp]),
     "vcb_pt_workspace_bytes": (i64, [i64]),
     "vcb_pathtrace_frame": (i32, [C.POINTER(VcbFrameParams), C.POINTER(VcbPtParams), vp]),
+    "vcb_debug_pt_math": (i32, [i64, vp, vp, vp, vp, vp, vp]),
+    "vcb_trace_free_flight": (i32, [C.POINTER(VcbFrameParams), C.POINTER(VcbPtParams), i64, vp, vp, vp, vp, vp, vp,
+                                    vp, vp]),
     "vcb_march_timing": (i32, [i32, vp, vp]),
     "vcb_last_launch_count": (i64, []),
     "vcb_frame_trace": (i32, [vp, i64, i32, i32, vp, vp]),

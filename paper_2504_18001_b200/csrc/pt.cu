@@ -316,7 +316,8 @@ __device__ __forceinline__ void pt_chunk(long long n, long long& lo, long long& 
 
 // ------------------------------------------------------------------ one walk step
 struct PtWalk {
-    const int* n_dev;
+    const int* n_dev;  // ray count on the device, or nullptr: n_const
+    long long n_const;
     const double* o;  // per ray [3n] when o_stride == 3, else oc
     const double* d;
     const double* t0;
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     int* cnt2 = s.cnt + 2 * kPtMaxCtas;
 
     // ---- init: walking = t < t_end (line 48), ordered list of walking rays
-    const long long n = __ldcg(wk.n_dev);
+    const long long n = wk.n_dev ? (long long)__ldcg(wk.n_dev) : wk.n_const;
     long long lo, hi;
     pt_chunk(n, lo, hi);
     {
@@ -786,6 +787,32 @@ __global__ void k_pt_finalize(VcbFrameParams p, VcbPtParams q, FrameWs fw, PtWs 
     }
 }
 
+__global__ void k_pt_walk_stats(VcbFrameParams p, PtWs s) {
+    p.stats->iterations = s.rng->iters;
+    p.stats->nonfinite = s.rng->nonfinite;
+}
+
+// diagnostics: log1p(x[i]) and the uniform of PCG64 draw idx[i] of the stream at pcg
+__global__ void k_pt_debug_math(int64_t n, const double* x, double* lg, u64 s_lo, u64 s_hi, u64 i_lo, u64 i_hi,
+                                const u64* idx, double* uni) {
+    __shared__ PtJump J[64];
+    if (threadIdx.x == 0) {
+        u128 m = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+        u128 c = ((u128)i_hi << 64) | i_lo;
+        for (int j = 0; j < 64; j++) {
+            J[j] = PtJump{(u64)m, (u64)(m >> 64), (u64)c, (u64)(c >> 64)};
+            c = (m + 1) * c;
+            m = m * m;
+        }
+    }
+    __syncthreads();
+    const u128 s0 = ((u128)s_hi << 64) | s_lo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lg[i] = pt_log1p(x[i]);
+        uni[i] = pcg_uniform_at(s0, idx[i], J);
+    }
+}
+
 void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
 extern thread_local long long g_launches;
 
@@ -800,6 +827,78 @@ static const void* pt_kernel(int mode) {
 using namespace cinr;
 
 extern "C" int64_t vcb_pt_workspace_bytes(int64_t max_rays) { return pt_ws_layout(max_rays, nullptr, nullptr); }
+
+// trace_free_flight (pathtrace.py:28-98) on caller rays: one walk, results copied out.
+extern "C" int32_t vcb_trace_free_flight(const VcbFrameParams* pp, const VcbPtParams* qq, int64_t n, const double* o,
+                                         const double* d, const double* t0, const double* t1, double* t_hit,
+                                         float* v_hit, uint64_t* draws, void* stream_) {
+    const VcbFrameParams& p = *pp;
+    const VcbPtParams& q = *qq;
+    cudaStream_t st = (cudaStream_t)stream_;
+    if (n < 0 || n > 0x7fffffff) return set_error("trace_free_flight: %lld rays", (long long)n);
+    if (q.n_tf < 2 || q.n_tf > kPtMaxTf) return set_error("trace_free_flight: %d transfer-function points", q.n_tf);
+    PtWs s;
+    const int64_t need = pt_ws_layout(n, q.workspace, &s);
+    if (need > q.workspace_bytes)
+        return set_error("trace_free_flight: workspace too small (%lld < %lld)", (long long)q.workspace_bytes,
+                         (long long)need);
+    const int mode = inr_mode(p.field);
+    const void* fn = pt_kernel(mode);
+    int smem = 0;
+    if (p.field.kind == 0) {
+        int nw = 0, nb = 0;
+        for (int L = 0; L < p.field.n_layers; L++) {
+            nw += p.field.widths[L] * p.field.widths[L + 1];
+            nb += p.field.widths[L + 1];
+        }
+        smem = (nw + nb) * 4;
+    }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int G = device_sms();
+    if (G > kPtMaxCtas) G = kPtMaxCtas;
+    if (n > 0) cudaMemsetAsync(s.lane_gen, 0xFF, (size_t)n * 4, st);
+    cudaMemsetAsync(s.cnt, 0, (size_t)4 * kPtMaxCtas * 4, st);
+    cudaMemsetAsync(s.bar, 0, 64, st);
+    k_pt_init<<<1, 32, 0, st>>>(q, s);
+    PtWalk wk = {};
+    wk.n_const = n;
+    wk.o = o;
+    wk.o_stride = 3;
+    wk.d = d;
+    wk.d_stride = 3;
+    wk.t0 = t0;
+    wk.t0_stride = 1;
+    wk.tend = t1;
+    wk.which = 1;
+    VcbFrameParams pc = p;
+    VcbPtParams qc = q;
+    FrameWs wc = {};
+    PtWs sc = s;
+    void* args[5] = {&pc, &qc, &wc, &sc, &wk};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, G, kPtThreads, args, smem, st);
+    if (e != cudaSuccess)
+        return set_error("trace_free_flight: cooperative launch (%d CTAs): %s", G, cudaGetErrorString(e));
+    k_pt_walk_stats<<<1, 1, 0, st>>>(p, s);
+    if (n > 0) {
+        cudaMemcpyAsync(t_hit, s.thit[1], (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(v_hit, s.vhit[1], (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    }
+    unsigned long long dr = 0;
+    cudaMemcpyAsync(&dr, &s.rng->draws, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e2 != cudaSuccess) return set_error("trace_free_flight: %s", cudaGetErrorString(e2));
+    if (draws) *draws = dr;
+    g_launches = 2;
+    return check_launch("trace_free_flight");
+}
+
+extern "C" int32_t vcb_debug_pt_math(int64_t n, const double* x, double* log1p_out, const uint64_t* pcg,
+                                     const uint64_t* draw_idx, double* uniform_out, void* stream) {
+    if (n <= 0) return 0;
+    k_pt_debug_math<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, log1p_out, pcg[0], pcg[1], pcg[2], pcg[3],
+                                                                         (const u64*)draw_idx, uniform_out);
+    return check_launch("debug_pt_math");
+}
 
 extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtParams* qq, void* stream_) {
     const VcbFrameParams& p = *pp;

@@ -239,7 +239,7 @@ class RenderSession:
         p.workspace_bytes = self._ws.numel()
         return p
 
-    def _pt_params(self, p):
+    def _pt_params(self, p, pcg=None, n_rays=None):
         """pathtrace_frame's scalars (pathtrace.py:112-117, 101-104): the numpy PCG64
         stream of default_rng(splitmix64((seed & 0xFFFFFFFF) ^ frame)) as seeded state,
         the normalised light direction, the TF control points."""
@@ -256,17 +256,51 @@ class RenderSession:
             q.light[a] = float(light[a])
         q.n_tf = int(self._tfp.shape[0])
         q.tf = ptr(self._tfp)
-        st, inc = pcg64_seeded_state(splitmix64((cfg.seed & 0xFFFFFFFF) ^ self.frame))
+        if pcg is None:
+            pcg = pcg64_seeded_state(splitmix64((cfg.seed & 0xFFFFFFFF) ^ self.frame))
+        st, inc = pcg
         q.pcg_state[0], q.pcg_state[1] = st & MASK64, st >> 64
         q.pcg_inc[0], q.pcg_inc[1] = inc & MASK64, inc >> 64
         q.lane_seed = cfg.seed & MASK64
         q.lane_frame = self.frame
-        need = N.load().vcb_pt_workspace_bytes(int(p.cam.width) * int(p.cam.rows))
+        n_rays = int(p.cam.width) * int(p.cam.rows) if n_rays is None else int(n_rays)
+        need = N.load().vcb_pt_workspace_bytes(n_rays)
         if getattr(self, "_pt_ws", None) is None or self._pt_ws.numel() < need:
             self._pt_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         q.workspace = ptr(self._pt_ws)
         q.workspace_bytes = self._pt_ws.numel()
         return q
+
+    def trace_free_flight(self, origins, directions, t_start, t_end, rng):
+        """pathtrace.py:28-98 `trace_free_flight(scene, ...)` on this session's sampler,
+        macro grid and settings: delta-track each ray to its first real collision.
+        `rng` is a numpy Generator (PCG64); it is advanced by the draws the walk used,
+        exactly as the reference's calls would have.  Returns (t_hit, value) host arrays,
+        t_hit = +inf for rays that escape.  The sampler starts a fresh lane pool."""
+        st = rng.bit_generator.state
+        if st.get("bit_generator") != "PCG64":
+            raise ValueError("trace_free_flight needs a numpy PCG64 generator (np.random.default_rng)")
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.float64).reshape(-1, 3))
+        n = o.shape[0]
+        d = np.ascontiguousarray(np.broadcast_to(np.asarray(directions, dtype=np.float64), (n, 3)))
+        t0 = np.ascontiguousarray(np.broadcast_to(np.asarray(t_start, dtype=np.float64), (n,)))
+        t1 = np.ascontiguousarray(np.broadcast_to(np.asarray(t_end, dtype=np.float64), (n,)))
+        dev = [torch.from_numpy(np.array(a)).to(self.device) for a in (o, d, t0, t1)]
+        t_hit = torch.empty(n, dtype=torch.float64, device=self.device)
+        v_hit = torch.empty(n, dtype=torch.float32, device=self.device)
+        if self._img is None:
+            self._img = torch.empty((1, 1, 4), dtype=torch.float32, device=self.device)
+        draws = np.zeros(1, dtype=np.uint64)
+        with torch.cuda.stream(self.stream):
+            self._stats.zero_()
+            p = self._frame_params(self._img)
+            q = self._pt_params(p, pcg=(int(st["state"]["state"]), int(st["state"]["inc"])), n_rays=n)
+            N.call("vcb_trace_free_flight", C.byref(p), C.byref(q), n, *(ptr(a) for a in dev), ptr(t_hit),
+                   ptr(v_hit), draws.ctypes.data, stream_ptr(self.stream))
+        if int(self._stats[7].item()):
+            raise RenderError("miss resolution failed: inference produced non-finite outputs")
+        rng.bit_generator.advance(int(draws[0]))
+        return t_hit.cpu().numpy(), v_hit.cpu().numpy()
 
     def render_frame_device(self):
         """Render + maintenance on the session stream; returns the device image

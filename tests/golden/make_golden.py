@@ -16,6 +16,14 @@ Capture points (all read-only wrappers, nothing in the reference is modified):
     (scheduler.py:79), FrameStats (taken before tick_frame), the image.
   * op level: inputs/outputs of kernels.raygen/advance/probe/shade_pass
     (render/kernels.py:160, 316, 370, 426) during one frame.
+
+Path-tracing fixtures (pt_* sessions, pt_flight.npz) are generated with numpy's
+AVX-512 dispatch disabled, NPY_DISABLE_CPU_FEATURES="AVX512F AVX512CD AVX512VL
+AVX512BW AVX512DQ AVX512_SKX AVX512_CLX AVX512_CNL AVX512_ICL AVX512_SPR AVX512VNNI
+AVX512IFMA AVX512VBMI AVX512VBMI2 AVX512BITALG AVX512FP16 AVX512VPOPCNTDQ": the free
+flights use np.log1p (pathtrace.py:80), which numpy computes with SVML on AVX-512
+hosts and with libm's log1p elsewhere (the two differ by 1 ulp on ~7% of inputs).
+The fixtures pin the libm semantics, which the device follows.
 """
 
 from __future__ import annotations
