@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--uncached-steps", type=int, default=5, help="frames of the no-cache INR baseline (0 = skip)")
+    ap.add_argument("--pt-steps", type=int, default=5,
+                    help="frames of the path-trace mode (pathtrace.py, spp 1) cached and uncached (0 = skip)")
     ap.add_argument("--mp", default="auto", choices=["auto", "frames", "tiles"],
                     help="N>1: 'frames' = alternate-frame rendering (each GPU renders whole 1024^2 frames of the orbit "
                          "with its own cache, frames gathered over NCCL; weak scaling, the default), 'tiles' = sort-first "
@@ -364,6 +366,9 @@ def main():
     if not args.no_e2e:
         import gc
 
+        _ = None  # drop the warm-up frame; the loop holds one frame while rendering the next
+        sess.reserve_host_frames(2)
+
         gc.collect()
         gc.disable()  # no collector pauses inside the timed public-API frames
         walls = []
@@ -440,6 +445,40 @@ def main():
                             "through the INR inside the frame kernel (true-miss path)"}
         del usess
 
+    # ---- the paper's second FPS column: the path tracer (render/pathtrace.py) on the same
+    # model, orbit and cache configuration, cached and uncached, device-timed like `value`
+    pathtrace = None
+    if ctx.world == 1 and args.pt_steps > 0:
+        pathtrace = {"spp": 1, "note": "SessionConfig(mode='pathtrace', samples_per_pixel=1): delta-tracked primary "
+                                       "walk + one shadow ray per hit, numpy-PCG64-exact draws, same sampler/cache"}
+        for label, cached in (("cached", True), ("uncached", False)):
+            pcfg = SessionConfig(cached=cached, mode="pathtrace", samples_per_pixel=1, loader="inline",
+                                 cache=cfg.cache, scheduler=cfg.scheduler, policy=cfg.policy, settings=cfg.settings,
+                                 seed=0)
+            psess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), pcfg, macro=mg)
+            pst = psess.stream
+            pts, psamp, piters = [], 0, 0
+            for i in range(args.warmup + args.pt_steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(pst)
+                psess.set_camera(traj.camera_at(args.warmup + i))
+                t0 = time.perf_counter()
+                psess.render_frame_device()
+                e1.record(pst)
+                prec = psess.collect_record(t0)
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    pts.append(e0.elapsed_time(e1))
+                    psamp += prec.samples
+                    piters += psess.last_frame_stats.get("iterations", 0)
+            pathtrace[label] = {"fps": len(pts) / (sum(pts) / 1000.0), "ms_per_frame": statistics.mean(pts),
+                                "samples_per_frame": psamp / len(pts), "walk_iterations_per_frame": piters / len(pts),
+                                "frames": len(pts)}
+            del psess
+        pathtrace["cache_speedup"] = pathtrace["cached"]["fps"] / pathtrace["uncached"]["fps"]
+
     decode = None
     if ctx.rank == 0 and args.decode_n > 0:
         try:
@@ -470,6 +509,7 @@ def main():
                          "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,
                          "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "inr_decode": decode, "uncached_inr_baseline": uncached,
+            "pathtrace": pathtrace,
             "clocks": clk.summary(), "gpu_launches": launches,
             "samples_per_frame": samples_all / (args.steps * per_step),
             "inr_samples_per_frame": float(np.mean([r.true_misses for r in recs])) + 40 * 16 ** 3,

@@ -392,6 +392,15 @@ class RenderSession:
                 return t
         return torch.empty(shape, dtype=torch.float32, pin_memory=True)
 
+    def reserve_host_frames(self, k: int = 2):
+        """Pre-allocate k pinned host frames of the current camera's shape, so a loop
+        that holds the previous frame while rendering the next never allocates."""
+        H, W = int(self.camera.height), int(self.camera.width)
+        shape = (self._band_rows(H), W, 4)
+        have = sum(1 for t in self._pin_free if tuple(t.shape) == shape)
+        for _ in range(max(0, k - have)):
+            self._pin_free.append(torch.empty(shape, dtype=torch.float32, pin_memory=True))
+
     def march_kernel_time(self):
         """(ms, launches) of the ray-march kernel in the last timing=True frame."""
         ms = C.c_double(0.0)
