@@ -211,6 +211,28 @@ typedef struct {
     int64_t workspace_bytes;
 } VcbPtParams;
 
+/* INR training (inr/train.py:16-132): `steps` optimizer steps of MSE on batches of
+ * rng.random((batch, 3)) positions of numpy's PCG64 stream (default_rng(seed) state,
+ * draw0 draws already consumed), targets from the target field's decoder. */
+typedef struct {
+    VcbField model;          /* default 8x2 hash grid + 16-32-32-1 MLP; its device tables/weights/biases
+                                are updated in place */
+    VcbField target;         /* the field fitted (lattice / procedural / INR) */
+    int64_t batch, steps, step0;   /* step0 = optimizer steps already taken (Adam t) */
+    int32_t optimizer, pad_;       /* 0 = Adam (train.py:51-75), 1 = SGD (40-48) */
+    double lr, beta1, beta2, eps, clip_norm;   /* clip_norm <= 0: no clipping (78-85) */
+    uint64_t pcg_state[2], pcg_inc[2];
+    uint64_t draw0;
+    int64_t n_table_params, n_weights, n_params;  /* flat parameter order: tables, weights, biases */
+    double *grads, *m, *v;   /* [n_params] f64; grads zero on entry and left zero */
+    double *pos;             /* [batch][3] */
+    float *targets;          /* [batch] */
+    double *loss;            /* [steps] per-step sum of squared errors (zeroed by the caller) */
+    double *scratch;         /* [8] */
+    int32_t *nonfinite;      /* target-decode flag */
+    void *jump;              /* vcb_train_workspace_bytes(batch) bytes */
+} VcbTrainParams;
+
 const char *vcb_last_error(void);
 int32_t vcb_abi_version(void);
 int32_t vcb_device_sm_count(void);
@@ -257,6 +279,10 @@ int32_t vcb_update_majorants(const float *vmin, const float *vmax, int64_t n, co
 /* image_io.py:14-21 to_rgba8 on the device: out[i] = uint8(clip(f64(image[i]), 0, 1) * 255 + 0.5)
  * for the n_pixels RGBA f32 pixels of image (frame streaming, protocol.py:59-61). */
 int32_t vcb_frame_rgba8(const float *image, int64_t n_pixels, uint8_t *out, void *stream);
+
+/* ---- training ABI */
+int64_t vcb_train_workspace_bytes(int64_t batch);
+int32_t vcb_train_steps(const VcbTrainParams *p, void *stream);
 
 /* ---- session ABI */
 int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations);

@@ -28,6 +28,7 @@ SOURCES = {
     "wave3.cu": ["-fmad=false"],
     "wave4.cu": ["-fmad=false"],
     "pt.cu": ["-fmad=false"],
+    "train.cu": [],
     "decode.cu": [],
     "cache.cu": [],
     "decode_tc.cu": [],

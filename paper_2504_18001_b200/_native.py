@@ -101,6 +101,15 @@ class VcbPtParams(C.Structure):
                 ("lane_seed", C.c_uint64), ("lane_frame", i64), ("workspace", vp), ("workspace_bytes", i64)]
 
 
+class VcbTrainParams(C.Structure):
+    _fields_ = [("model", VcbField), ("target", VcbField), ("batch", i64), ("steps", i64), ("step0", i64),
+                ("optimizer", i32), ("pad_", i32), ("lr", f64), ("beta1", f64), ("beta2", f64), ("eps", f64),
+                ("clip_norm", f64), ("pcg_state", C.c_uint64 * 2), ("pcg_inc", C.c_uint64 * 2),
+                ("draw0", C.c_uint64), ("n_table_params", i64), ("n_weights", i64), ("n_params", i64),
+                ("grads", vp), ("m", vp), ("v", vp), ("pos", vp), ("targets", vp), ("loss", vp), ("scratch", vp),
+                ("nonfinite", vp), ("jump", vp)]
+
+
 _PROTOS = {
     "vcb_last_error": (C.c_char_p, []),
     "vcb_abi_version": (i32, []),
@@ -123,6 +132,8 @@ _PROTOS = {
     "vcb_pt_workspace_bytes": (i64, [i64]),
     "vcb_pathtrace_frame": (i32, [C.POINTER(VcbFrameParams), C.POINTER(VcbPtParams), vp]),
     "vcb_debug_pt_math": (i32, [i64, vp, vp, vp, vp, vp, vp]),
+    "vcb_train_workspace_bytes": (i64, [i64]),
+    "vcb_train_steps": (i32, [C.POINTER(VcbTrainParams), vp]),
     "vcb_trace_free_flight": (i32, [C.POINTER(VcbFrameParams), C.POINTER(VcbPtParams), i64, vp, vp, vp, vp, vp, vp,
                                     vp, vp]),
     "vcb_march_timing": (i32, [i32, vp, vp]),
@@ -168,7 +179,7 @@ def load():
 
 
 STRUCTS = (VcbCamera, VcbMarchStatic, VcbProbeStatic, VcbField, VcbBrickGeom, VcbFrameStats, VcbCacheState,
-           VcbFrameParams, VcbMaintParams, VcbPtParams)
+           VcbFrameParams, VcbMaintParams, VcbPtParams, VcbTrainParams)
 
 
 def struct_sizes():

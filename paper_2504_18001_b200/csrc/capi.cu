@@ -48,7 +48,7 @@ extern "C" int32_t vcb_struct_sizes(int64_t* out, int32_t n) {
     const int64_t s[] = {(int64_t)sizeof(VcbCamera),     (int64_t)sizeof(VcbMarchStatic), (int64_t)sizeof(VcbProbeStatic),
                          (int64_t)sizeof(VcbField),      (int64_t)sizeof(VcbBrickGeom),   (int64_t)sizeof(VcbFrameStats),
                          (int64_t)sizeof(VcbCacheState), (int64_t)sizeof(VcbFrameParams), (int64_t)sizeof(VcbMaintParams),
-                         (int64_t)sizeof(VcbPtParams)};
+                         (int64_t)sizeof(VcbPtParams), (int64_t)sizeof(VcbTrainParams)};
     const int k = (int)(sizeof(s) / sizeof(s[0]));
     for (int i = 0; i < n && i < k; i++) out[i] = s[i];
     return k;
