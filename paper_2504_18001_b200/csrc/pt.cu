@@ -24,7 +24,9 @@
 // Ranks come from per-CTA counts (each CTA owns a contiguous chunk of the active
 // list) plus a block scan, so every draw index, lane and list position equals the
 // reference's.  The PCG64 state of draw D is a jump of the seeded state by D + 1
-// steps (a table of (A^2^j, C_j) built on the device per frame); log1p is glibc's
+// steps (a radix-16 table of LCG jumps built on the device per frame: a CTA keeps the
+// state at the start of each 512-ray round and a lane jumps by its rank, at most three
+// table steps); log1p is glibc's
 // algorithm (the FMA build numpy calls on x86-64), bit-identical.
 #include <cstdio>
 
@@ -64,6 +66,7 @@ struct PtWs {
     float* vhit[2];
     int* list[2];
     uint8_t* flag;
+    uint8_t* flag2;    // second list-flag buffer (walk rebalancing)
     float* mub;        // [n] majorant of a settled ray's cell (mu[~empty][~crossed], line 91)
     double* sh_o;      // [3n] shadow origins (primary hit points)
     double* sh_tend;   // [n] t_far of the shadow ray
@@ -75,7 +78,8 @@ struct PtWs {
     int* cnt;          // [4][kPtMaxCtas]
     unsigned* bar;
     PtRng* rng;
-    PtJump* jump;      // [64]
+    PtJump* jump;      // [64] binary jump table (A^2^j, C_j)
+    PtJump* j16;       // [16][16] radix-16 jump table: digit d, value v -> jump by v*16^d
 };
 
 inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
@@ -93,6 +97,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
         o_l[b] = take((size_t)n * 4);
     }
     size_t o_f = take((size_t)n);
+    size_t o_f2 = take((size_t)n);
     size_t o_mub = take((size_t)n * 4);
     size_t o_sho = take((size_t)n * 24);
     size_t o_sht = take((size_t)n * 8);
@@ -105,6 +110,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
     size_t o_bar = take(64);
     size_t o_rng = take(sizeof(PtRng));
     size_t o_j = take(64 * sizeof(PtJump));
+    size_t o_j16 = take(256 * sizeof(PtJump));
     if (base && s) {
         char* p = (char*)base;
         for (int b = 0; b < 2; b++) {
@@ -114,6 +120,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
             s->list[b] = (int*)(p + o_l[b]);
         }
         s->flag = (uint8_t*)(p + o_f);
+        s->flag2 = (uint8_t*)(p + o_f2);
         s->mub = (float*)(p + o_mub);
         s->sh_o = (double*)(p + o_sho);
         s->sh_tend = (double*)(p + o_sht);
@@ -126,6 +133,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
         s->bar = (unsigned*)(p + o_bar);
         s->rng = (PtRng*)(p + o_rng);
         s->jump = (PtJump*)(p + o_j);
+        s->j16 = (PtJump*)(p + o_j16);
     }
     return (int64_t)align_up(off, 256);
 }
@@ -212,6 +220,26 @@ __device__ __forceinline__ double pcg_uniform_at(u128 s0, u64 d, const PtJump* _
             s = s * (((u128)e.m_hi << 64) | e.m_lo) + (((u128)e.p_hi << 64) | e.p_lo);
         }
     }
+    const u64 hi = (u64)(s >> 64), lo = (u64)s;
+    const u64 x = hi ^ lo;
+    const unsigned r = (unsigned)(hi >> 58);
+    const u64 out = (x >> r) | (x << ((64u - r) & 63u));
+    return (double)(out >> 11) * 1.1102230246251565e-16;  // 2^-53
+}
+
+// state jumped by delta steps with the radix-16 table (at most one step per hex digit)
+__device__ __forceinline__ u128 pcg_jump16(u128 s, u64 delta, const PtJump* J) {
+    for (int d = 0; delta; d++, delta >>= 4) {
+        const int v = (int)(delta & 15);
+        if (v) {
+            const PtJump e = J[d * 16 + v];
+            s = s * (((u128)e.m_hi << 64) | e.m_lo) + (((u128)e.p_hi << 64) | e.p_lo);
+        }
+    }
+    return s;
+}
+
+__device__ __forceinline__ double pcg_out(u128 s) {
     const u64 hi = (u64)(s >> 64), lo = (u64)s;
     const u64 x = hi ^ lo;
     const unsigned r = (unsigned)(hi >> 58);
@@ -306,6 +334,48 @@ __device__ __forceinline__ void pt_cta_prefix(const int* cnt, long long* s, long
     __syncthreads();
 }
 
+// prefix + total + max of a per-CTA count array
+__device__ __forceinline__ void pt_cta_prefix_max(const int* cnt, long long* s, long long& pre, long long& tot,
+                                                  long long& mx) {
+    long long a = 0, b = 0, c = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const int v = __ldcg(cnt + i);
+        b += v;
+        c = v > c ? v : c;
+        if (i < (int)blockIdx.x) a += v;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long y = __shfl_xor_sync(0xffffffffu, c, o);
+        c = y > c ? y : c;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s[3 * warp] = a;
+        s[3 * warp + 1] = b;
+        s[3 * warp + 2] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long x = 0, y = 0, z = 0;
+        for (int w = 0; w < kPtThreads / 32; w++) {
+            x += s[3 * w];
+            y += s[3 * w + 1];
+            z = s[3 * w + 2] > z ? s[3 * w + 2] : z;
+        }
+        s[64] = x;
+        s[65] = y;
+        s[66] = z;
+    }
+    __syncthreads();
+    pre = s[64];
+    tot = s[65];
+    mx = s[66];
+    __syncthreads();
+}
+
 __device__ __forceinline__ void pt_chunk(long long n, long long& lo, long long& hi) {
     const long long ch = (n + gridDim.x - 1) / gridDim.x;
     lo = (long long)blockIdx.x * ch;
@@ -367,7 +437,91 @@ __device__ __forceinline__ PtGeo pt_geo(const VcbFrameParams& p, float dens_f, d
     return g;
 }
 
+// VolumeSampler.sample for one settled ray at rank `lane` of its batch (sampler.py:196-280):
+// lane RNG (lazily reseeded generations), |pos - camera| distance, MRPD probe + stamp,
+// miss filing at the requested LoD, true-miss inference at clamp_normalized(pos).
+template <int kInr>
+__device__ __forceinline__ float pt_sample(const VcbFrameParams& p, const PtWs& s, const PtRng& R, const MlpSmem& mlp,
+                                           long long lane, double px, double py, double pz,
+                                           unsigned long long& c_ex, unsigned long long& c_fb,
+                                           unsigned long long& c_ms) {
+    const double hi_n = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
+    float v = 0.0f;
+    bool miss = true;
+    if (p.cached) {
+        double u = 0.0;
+        if (p.probe.mode != 2) {
+            uint32_t st = (__ldcg(s.lane_gen + lane) == R.gen) ? __ldcg(s.lane_st + lane) : lane_seed(R.base, (u64)lane);
+            st = xorshift32(st);
+            __stcg(s.lane_st + lane, st);
+            __stcg(s.lane_gen + lane, R.gen);
+            u = DMUL((double)st, 2.3283064365386963e-10);
+        }
+        const double ex = DSUB(px, p.cam.origin[0]), ey = DSUB(py, p.cam.origin[1]), ez = DSUB(pz, p.cam.origin[2]);
+        const double dist = __dsqrt_rn(DADD(DADD(DMUL(ex, ex), DMUL(ey, ey)), DMUL(ez, ez)));
+        int rq, slot;
+        const int sv = probe_one(px, py, pz, dist, u, p.probe, p.table, p.pool, (long long*)p.last_used,
+                                 p.cache_frame, v, rq, slot);
+        if (sv != rq) {
+            // mrpd.py:215-225 miss filing at the requested LoD (native clipped)
+            const i64 span = p.probe.b << rq;
+            const double nx = clampd(DSUB(DMUL(px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
+            const double ny = clampd(DSUB(DMUL(py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
+            const double nz = clampd(DSUB(DMUL(pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
+            const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, p.probe.grid[rq][0] - 1);
+            const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, p.probe.grid[rq][1] - 1);
+            const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, p.probe.grid[rq][2] - 1);
+            warp_aggregated_add(p.miss_count,
+                                p.probe.offset[rq] + bx + p.probe.grid[rq][0] * (by + p.probe.grid[rq][1] * bz));
+        }
+        miss = sv < 0;
+        if (!miss) {
+            c_ex += (sv == rq);
+            c_fb += (sv != rq);
+        }
+    }
+    if (miss) {
+        c_ms++;
+        v = field_eval<kInr>(p.field, clampd(px, 0.0, hi_n), clampd(py, 0.0, hi_n), clampd(pz, 0.0, hi_n), mlp,
+                             &s.rng->nonfinite);
+    }
+    return v;
+}
+
+// shadow ray j of primary ray i hit at th: origin o + d th, t_far = intersect_aabb(points,
+// light)[1] (camera.py:95-110, pathtrace.py:101-108)
+template <class FO, class FD>
+__device__ __forceinline__ void pt_shadow_ray(const VcbPtParams& q, const PtWs& s, long long j, int i, double th,
+                                              FO& ray_o, FD& ray_d) {
+    double ox, oy, oz, dx, dy, dz;
+    ray_o(i, ox, oy, oz);
+    ray_d(i, dx, dy, dz);
+    const double px = DADD(ox, DMUL(dx, th)), py = DADD(oy, DMUL(dy, th)), pz = DADD(oz, DMUL(dz, th));
+    s.sh_o[3 * j] = px;
+    s.sh_o[3 * j + 1] = py;
+    s.sh_o[3 * j + 2] = pz;
+    const double o3[3] = {px, py, pz};
+    double tfar = INFINITY;
+    for (int a = 0; a < 3; a++) {
+        const double da = q.light[a];
+        double tl, th2;
+        if (da != 0.0) {
+            const double inv = __ddiv_rn(1.0, da);
+            tl = DMUL(DSUB(0.0, o3[a]), inv);
+            th2 = DMUL(DSUB(1.0, o3[a]), inv);
+        } else {
+            const bool inside = o3[a] >= 0.0 && o3[a] <= 1.0;
+            tl = inside ? -INFINITY : INFINITY;
+            th2 = inside ? INFINITY : -INFINITY;
+        }
+        const double mx = tl > th2 ? tl : th2;
+        tfar = (a == 0 || mx < tfar) ? mx : tfar;
+    }
+    s.sh_tend[j] = tfar;
+}
+
 struct PtSmem {
+    PtJump j16[256];
     double tf[kPtMaxTf * 5];
     long long red[70];
     int w[40];
@@ -381,6 +535,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     MlpSmem mlp;
     if (kInr != 0) stage_mlp(p.field, smem, mlp);
     for (int i = threadIdx.x; i < q.n_tf * 5; i += blockDim.x) sm.tf[i] = q.tf[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.j16[i] = s.j16[i];
     unsigned target = 0;
     const int W = wk.which;
     double* T = s.t[W];
@@ -393,6 +548,8 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     const u128 s0 = ((u128)q.pcg_state[1] << 64) | q.pcg_state[0];
     unsigned long long c_req = 0, c_ex = 0, c_fb = 0, c_ms = 0;
     __syncthreads();
+    // PCG64 state after the R.draws draws consumed so far (draw x = out(state after x+1 steps))
+    u128 SD = pcg_jump16(s0, R.draws, sm.j16);
 
     auto ray_o = [&](int r, double& x, double& y, double& z) {
         if (wk.o_stride) {
@@ -488,6 +645,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
         // phase 2: free-flight draws of the dense rays (77-88)
         {
             int cnt = 0;
+            u128 Sr = pcg_jump16(SD, (u64)pre_d, sm.j16);  // state before this round's first draw
             for (long long b0 = lo; b0 < hi; b0 += blockDim.x) {
                 const long long i = b0 + threadIdx.x;
                 uint8_t cls = 0;
@@ -504,7 +662,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                     ray_d(r, dx, dy, dz);
                     const double t = __ldcg(T + r), te = __ldcg(wk.tend + r);
                     const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te);
-                    const double xi = pcg_uniform_at(s0, R.draws + (u64)(pre_d + rk), s.jump);
+                    const double xi = pcg_out(pcg_jump16(Sr, (u64)rk + 1, sm.j16));
                     const double tc = DSUB(t, __ddiv_rn(pt_log1p(-xi), (double)g.mu));
                     if (tc >= g.exit_t) {
                         if (g.at_end) {
@@ -522,6 +680,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                     __stcg(s.flag + i, cls);
                 }
                 pre_d += tot;
+            Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
             }
             cnt = warp_sum(cnt);
             if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(cnt2 + blockIdx.x, cnt);
@@ -548,7 +707,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
         // phase 3: sample the settled rays, accept or reject (89-97)
         {
             int cnt = 0;
-            const bool use_rng = p.cached && p.probe.mode != 2;
+            u128 Sr = pcg_jump16(SD, (u64)(n_dense + pre_s), sm.j16);
             for (long long b0 = lo; b0 < hi; b0 += blockDim.x) {
                 const long long i = b0 + threadIdx.x;
                 uint8_t cls = 0;
@@ -565,56 +724,12 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                     ray_d(r, dx, dy, dz);
                     const double t = __ldcg(T + r);
                     const double px = DADD(ox, DMUL(dx, t)), py = DADD(oy, DMUL(dy, t)), pz = DADD(oz, DMUL(dz, t));
-                    float v = 0.0f;
-                    bool miss = true;
                     c_req++;
-                    if (p.cached) {
-                        double u = 0.0;
-                        const long long lane = pre_s + rk;
-                        if (use_rng) {
-                            uint32_t st = (__ldcg(s.lane_gen + lane) == R.gen) ? __ldcg(s.lane_st + lane)
-                                                                               : lane_seed(R.base, (u64)lane);
-                            st = xorshift32(st);
-                            __stcg(s.lane_st + lane, st);
-                            __stcg(s.lane_gen + lane, R.gen);
-                            u = DMUL((double)st, 2.3283064365386963e-10);
-                        }
-                        const double ex = DSUB(px, p.cam.origin[0]), ey = DSUB(py, p.cam.origin[1]),
-                                     ez = DSUB(pz, p.cam.origin[2]);
-                        const double dist = __dsqrt_rn(DADD(DADD(DMUL(ex, ex), DMUL(ey, ey)), DMUL(ez, ez)));
-                        int rq, slot;
-                        const int sv = probe_one(px, py, pz, dist, u, p.probe, p.table, p.pool,
-                                                 (long long*)p.last_used, p.cache_frame, v, rq, slot);
-                        if (sv != rq) {
-                            // mrpd.py:215-225 miss filing at the requested LoD (native clipped)
-                            const i64 span = p.probe.b << rq;
-                            const double nx = clampd(DSUB(DMUL(px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
-                            const double ny = clampd(DSUB(DMUL(py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
-                            const double nz = clampd(DSUB(DMUL(pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
-                            const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][0] - 1);
-                            const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][1] - 1);
-                            const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][2] - 1);
-                            warp_aggregated_add(p.miss_count, p.probe.offset[rq] + bx +
-                                                                  p.probe.grid[rq][0] * (by + p.probe.grid[rq][1] * bz));
-                        }
-                        miss = sv < 0;
-                        if (!miss) {
-                            c_ex += (sv == rq);
-                            c_fb += (sv != rq);
-                        }
-                    }
-                    if (miss) {
-                        c_ms++;
-                        v = field_eval<kInr>(p.field, clampd(px, 0.0, hi_n), clampd(py, 0.0, hi_n),
-                                             clampd(pz, 0.0, hi_n), mlp, &s.rng->nonfinite);
-                    }
+                    const float v = pt_sample<kInr>(p, s, R, mlp, pre_s + rk, px, py, pz, c_ex, c_fb, c_ms);
                     // sigma = tf.opacity(values) * pt_density; accept = xi < sigma / mu
                     const double vv = clampd((double)v, 0.0, 1.0);
                     const double sig = DMUL(np_interp(vv, sm.tf, sm.tf + 4, q.n_tf, 5), q.density);
-                    const double xi = pcg_uniform_at(s0, R.draws + (u64)(n_dense + pre_s + rk), s.jump);
+                    const double xi = pcg_out(pcg_jump16(Sr, (u64)rk + 1, sm.j16));
                     if (xi < __ddiv_rn(sig, (double)__ldcg(s.mub + i))) {
                         __stcg(TH + r, t);
                         __stcg(VH + r, v);
@@ -627,11 +742,13 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                 if (i < hi) __stcg(s.flag + i, cls);
                 cnt += cls;
                 pre_s += tot;
+                Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
             }
             cnt = warp_sum(cnt);
             if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(cnt0 + blockIdx.x, cnt);
         }
         R.draws += (u64)(n_dense + n_set);
+        SD = pcg_jump16(SD, (u64)(n_dense + n_set), sm.j16);
         pt_barrier(s.bar, target);
         long long pre_v, m_next;
         pt_cta_prefix(cnt0, sm.red, pre_v, m_next);
@@ -683,35 +800,319 @@ __global__ void __launch_bounds__(kPtThreads, 1)
             int tot;
             const int rk = pt_block_rank(f, sm.w, tot);
             if (i < hi) s.sh_of[i] = f ? (int)(pre_h + rk) : -1;
-            if (f) {
-                const long long j = pre_h + rk;
-                double ox, oy, oz, dx, dy, dz;
-                ray_o((int)i, ox, oy, oz);
-                ray_d((int)i, dx, dy, dz);
-                const double px = DADD(ox, DMUL(dx, th)), py = DADD(oy, DMUL(dy, th)), pz = DADD(oz, DMUL(dz, th));
-                s.sh_o[3 * j] = px;
-                s.sh_o[3 * j + 1] = py;
-                s.sh_o[3 * j + 2] = pz;
-                // intersect_aabb(points, light)[1] (camera.py:95-110)
-                const double o3[3] = {px, py, pz};
-                double tfar = INFINITY;
-                for (int a = 0; a < 3; a++) {
-                    const double da = q.light[a];
-                    double tl, th2;
-                    if (da != 0.0) {
-                        const double inv = __ddiv_rn(1.0, da);
-                        tl = DMUL(DSUB(0.0, o3[a]), inv);
-                        th2 = DMUL(DSUB(1.0, o3[a]), inv);
-                    } else {
-                        const bool inside = o3[a] >= 0.0 && o3[a] <= 1.0;
-                        tl = inside ? -INFINITY : INFINITY;
-                        th2 = inside ? INFINITY : -INFINITY;
-                    }
-                    const double mx = tl > th2 ? tl : th2;
-                    tfar = (a == 0 || mx < tfar) ? mx : tfar;
-                }
-                s.sh_tend[j] = tfar;
+            if (f) pt_shadow_ray(q, s, pre_h + rk, (int)i, th, ray_o, ray_d);
+            pre_h += tot;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) s.rng->sh_n = (int)n_h;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s.rng->draws = R.draws;
+        s.rng->pool = R.pool;
+        s.rng->salt = R.salt;
+        s.rng->gen = R.gen;
+        s.rng->base = R.base;
+        s.rng->iters = R.iters;
+    }
+}
+
+
+__device__ __forceinline__ int pt_block_sum(int v, int* s_w) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = 0;
+    for (int w = 0; w < kPtThreads / 32; w++) t += s_w[w];
+    __syncthreads();
+    return t;
+}
+
+// Two grid barriers per wavefront iteration (walk schedule 1).  Each CTA owns a
+// contiguous range of the walk's rays for the whole walk and keeps the ones still
+// walking in its own segment of the list, in ray order, so the global order is CTA
+// order then list order and a rank is (counts of the CTAs before) + (block rank).
+//   barrier A: dense counts of this iteration published
+//   draws:     free flights of the dense rays (draw D + dense rank)
+//   barrier B: settled counts published
+//   sample:    settled rays sampled + accepted (lane = settled rank, draw D + n_dense +
+//              settled rank); then, fused, walking &= t < t_end, the in-place compaction
+//              of the CTA's list and the classification of the next iteration (outside,
+//              majorant, cell exit; empty cells hop), whose dense count is published
+// Rays that the next classification retires (outside / escaping an empty cell) leave
+// the list one iteration early; they draw nothing, so every draw, lane and value is
+// the reference's.
+template <int kInr>
+__global__ void __launch_bounds__(kPtThreads, 1)
+    k_pt_walk2(VcbFrameParams p, VcbPtParams q, FrameWs fw, PtWs s, PtWalk wk) {
+    __shared__ PtSmem sm;
+    extern __shared__ __align__(16) float smem[];
+    MlpSmem mlp;
+    if (kInr != 0) stage_mlp(p.field, smem, mlp);
+    for (int i = threadIdx.x; i < q.n_tf * 5; i += blockDim.x) sm.tf[i] = q.tf[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.j16[i] = s.j16[i];
+    unsigned target = 0;
+    const int W = wk.which;
+    double* T = s.t[W];
+    double* TH = s.thit[W];
+    float* VH = s.vhit[W];
+    const float dens_f = __double2float_rn(q.density);
+    PtRng R = *s.rng;
+    const u128 s0 = ((u128)q.pcg_state[1] << 64) | q.pcg_state[0];
+    unsigned long long c_req = 0, c_ex = 0, c_fb = 0, c_ms = 0;
+    __syncthreads();
+    // PCG64 state after the R.draws draws consumed so far (draw x = out(state after x+1 steps))
+    u128 SD = pcg_jump16(s0, R.draws, sm.j16);
+    auto ray_o = [&](int r, double& x, double& y, double& z) {
+        if (wk.o_stride) {
+            x = __ldcg(wk.o + 3 * r);
+            y = __ldcg(wk.o + 3 * r + 1);
+            z = __ldcg(wk.o + 3 * r + 2);
+        } else {
+            x = wk.oc[0];
+            y = wk.oc[1];
+            z = wk.oc[2];
+        }
+    };
+    auto ray_d = [&](int r, double& x, double& y, double& z) {
+        if (wk.d_stride) {
+            x = __ldcg(wk.d + 3 * r);
+            y = __ldcg(wk.d + 3 * r + 1);
+            z = __ldcg(wk.d + 3 * r + 2);
+        } else {
+            x = wk.dc[0];
+            y = wk.dc[1];
+            z = wk.dc[2];
+        }
+    };
+    // pathtrace.py:54-75 for ray r at parameter t: 0 retired, 1 hopped (t moved), 2 dense
+    auto classify = [&](int r, double t) -> uint8_t {
+        double ox, oy, oz, dx, dy, dz;
+        ray_o(r, ox, oy, oz);
+        ray_d(r, dx, dy, dz);
+        const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, __ldcg(wk.tend + r));
+        if (g.outside) return 0;
+        if (g.mu > 0.0f) return 2;
+        if (g.at_end) return 0;
+        __stcg(T + r, DADD(g.exit_t, 1e-9));
+        return 1;
+    };
+    int* cntD = s.cnt;
+    int* cntS = s.cnt + kPtMaxCtas;
+    int* cntL = s.cnt + 2 * kPtMaxCtas;
+    int* cntH = s.cnt + 3 * kPtMaxCtas;
+    const long long n = wk.n_dev ? (long long)__ldcg(wk.n_dev) : wk.n_const;
+    long long own_lo, own_hi;
+    pt_chunk(n, own_lo, own_hi);
+    int cur = 0;  // list / flag buffer generation (flips on a rebalance)
+    int* L = s.list[0] + own_lo;
+    uint8_t* FL = s.flag + own_lo;
+    float* MU = s.mub + own_lo;
+    // init (line 44-48) + classification of iteration 0
+    long long len = 0;
+    int nd = 0;
+    for (long long b0 = own_lo; b0 < own_hi; b0 += blockDim.x) {
+        const long long i = b0 + threadIdx.x;
+        uint8_t cls = 0;
+        if (i < own_hi) {
+            const double t0 = wk.t0_stride ? __ldcg(wk.t0 + i) : wk.t0c;
+            __stcg(T + i, t0);
+            __stcg(TH + i, (double)INFINITY);
+            __stcg(VH + i, 0.0f);
+            if (t0 < __ldcg(wk.tend + i)) cls = classify((int)i, t0);
+        }
+        int tot;
+        const int rk = pt_block_rank(cls != 0, sm.w, tot);
+        if (cls) {
+            __stcg(L + len + rk, (int)i);
+            __stcg(FL + len + rk, cls);
+        }
+        nd += cls == 2;
+        len += tot;
+    }
+    nd = pt_block_sum(nd, sm.w);
+    if (threadIdx.x == 0) {
+        cntD[blockIdx.x] = nd;
+        cntL[blockIdx.x] = (int)len;
+    }
+    long long k = 0;
+    for (;; k++) {
+        pt_barrier(s.bar, target);  // A
+        long long pre_d, n_dense, pre_l, m, maxl;
+        pt_cta_prefix(cntD, sm.red, pre_d, n_dense);
+        pt_cta_prefix_max(cntL, sm.red, pre_l, m, maxl);
+        if (m == 0 || k >= q.max_walk) break;
+        const long long ch = (m + gridDim.x - 1) / gridDim.x;
+        if ((maxl + kPtThreads - 1) / kPtThreads > (ch + kPtThreads - 1) / kPtThreads) {
+            // rebalance: the lists, concatenated in CTA order (= ray order), re-split evenly
+            int* Lb = s.list[cur ^ 1];
+            uint8_t* FLb = cur ? s.flag : s.flag2;
+            for (long long j = threadIdx.x; j < len; j += blockDim.x) {
+                __stcg(Lb + pre_l + j, __ldcg(L + j));
+                __stcg(FLb + pre_l + j, __ldcg(FL + j));
             }
+            pt_barrier(s.bar, target);
+            cur ^= 1;
+            long long lo2 = (long long)blockIdx.x * ch;
+            if (lo2 > m) lo2 = m;
+            long long hi2 = lo2 + ch;
+            if (hi2 > m) hi2 = m;
+            L = Lb + lo2;
+            FL = FLb + lo2;
+            MU = s.mub + lo2;
+            len = hi2 - lo2;
+            int nd2 = 0;
+            for (long long j = threadIdx.x; j < len; j += blockDim.x) nd2 += __ldcg(FL + j) == 2;
+            nd2 = pt_block_sum(nd2, sm.w);
+            if (threadIdx.x == 0) cntD[blockIdx.x] = nd2;
+            pt_barrier(s.bar, target);
+            pt_cta_prefix(cntD, sm.red, pre_d, n_dense);
+        }
+        // free flights of the dense rays (77-88)
+        int ns = 0;
+        u128 Sr = pcg_jump16(SD, (u64)pre_d, sm.j16);  // state before this round's first draw
+        for (long long b0 = 0; b0 < len; b0 += blockDim.x) {
+            const long long j = b0 + threadIdx.x;
+            uint8_t cls = 0;
+            int r = 0;
+            if (j < len) {
+                cls = __ldcg(FL + j);
+                r = __ldcg(L + j);
+            }
+            int tot;
+            const int rk = pt_block_rank(cls == 2, sm.w, tot);
+            if (cls == 2) {
+                double ox, oy, oz, dx, dy, dz;
+                ray_o(r, ox, oy, oz);
+                ray_d(r, dx, dy, dz);
+                const double t = __ldcg(T + r), te = __ldcg(wk.tend + r);
+                const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te);
+                const double xi = pcg_out(pcg_jump16(Sr, (u64)rk + 1, sm.j16));
+                const double tc = DSUB(t, __ddiv_rn(pt_log1p(-xi), (double)g.mu));
+                if (tc >= g.exit_t) {
+                    if (g.at_end) {
+                        cls = 0;
+                    } else {
+                        __stcg(T + r, DADD(g.exit_t, 1e-9));
+                        cls = 1;
+                    }
+                } else {
+                    __stcg(T + r, tc);
+                    __stcg(MU + j, g.mu);
+                    cls = 3;
+                    ns++;
+                }
+                __stcg(FL + j, cls);
+            }
+            pre_d += tot;
+            Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
+        }
+        ns = pt_block_sum(ns, sm.w);
+        if (threadIdx.x == 0) cntS[blockIdx.x] = ns;
+        pt_barrier(s.bar, target);  // B
+        long long pre_s, n_set;
+        pt_cta_prefix(cntS, sm.red, pre_s, n_set);
+        // VolumeSampler.sample lane pool (sampler.py:206-213)
+        if (n_set > 0) {
+            if (R.pool == 0) {
+                R.pool = n_set;
+                R.salt = 0;
+                R.gen += 1;
+                R.base = splitmix64((u64)q.lane_seed ^ ((u64)q.lane_frame * 0x9E3779B97F4A7C15ull));
+            } else if (R.pool < n_set) {
+                R.salt += 1;
+                R.pool = n_set;
+                R.gen += 1;
+                const u64 fr = (u64)q.lane_frame * 1000003ull + (u64)R.salt;
+                R.base = splitmix64((u64)q.lane_seed ^ (fr * 0x9E3779B97F4A7C15ull));
+            }
+        }
+        // sample + accept (89-97), walking &= t < t_end, compaction, next classification
+        long long new_len = 0;
+        Sr = pcg_jump16(SD, (u64)(n_dense + pre_s), sm.j16);
+        nd = 0;
+        for (long long b0 = 0; b0 < len; b0 += blockDim.x) {
+            const long long j = b0 + threadIdx.x;
+            uint8_t cls = 0;
+            int r = 0;
+            if (j < len) {
+                cls = __ldcg(FL + j);
+                r = __ldcg(L + j);
+            }
+            int tot;
+            const int rk = pt_block_rank(cls == 3, sm.w, tot);
+            if (cls == 3) {
+                double ox, oy, oz, dx, dy, dz;
+                ray_o(r, ox, oy, oz);
+                ray_d(r, dx, dy, dz);
+                const double t = __ldcg(T + r);
+                const double px = DADD(ox, DMUL(dx, t)), py = DADD(oy, DMUL(dy, t)), pz = DADD(oz, DMUL(dz, t));
+                c_req++;
+                const float v = pt_sample<kInr>(p, s, R, mlp, pre_s + rk, px, py, pz, c_ex, c_fb, c_ms);
+                const double vv = clampd((double)v, 0.0, 1.0);
+                const double sig = DMUL(np_interp(vv, sm.tf, sm.tf + 4, q.n_tf, 5), q.density);
+                const double xi = pcg_out(pcg_jump16(Sr, (u64)rk + 1, sm.j16));
+                if (xi < __ddiv_rn(sig, (double)__ldcg(MU + j))) {
+                    __stcg(TH + r, t);
+                    __stcg(VH + r, v);
+                    cls = 0;
+                } else {
+                    cls = 1;
+                }
+            }
+            uint8_t nc = 0;
+            if (cls == 1) {
+                const double t = __ldcg(T + r);
+                if (t < __ldcg(wk.tend + r)) nc = classify(r, t);
+            }
+            int tot2;
+            const int rk2 = pt_block_rank(nc != 0, sm.w, tot2);  // all reads of L/FL/MU above precede it
+            if (nc) {
+                __stcg(L + new_len + rk2, r);
+                __stcg(FL + new_len + rk2, nc);
+            }
+            nd += nc == 2;
+            new_len += tot2;
+            pre_s += tot;
+            Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
+        }
+        R.draws += (u64)(n_dense + n_set);
+        SD = pcg_jump16(SD, (u64)(n_dense + n_set), sm.j16);
+        len = new_len;
+        nd = pt_block_sum(nd, sm.w);
+        if (threadIdx.x == 0) {
+            cntD[blockIdx.x] = nd;
+            cntL[blockIdx.x] = (int)len;
+        }
+    }
+    R.iters += k;
+    c_req = warp_sum(c_req);
+    c_ex = warp_sum(c_ex);
+    c_fb = warp_sum(c_fb);
+    c_ms = warp_sum(c_ms);
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(p.stats);
+        if (c_req) atomicAdd(st + 0, c_req);
+        if (c_ex) atomicAdd(st + 1, c_ex);
+        if (c_fb) atomicAdd(st + 2, c_fb);
+        if (c_ms) atomicAdd(st + 3, c_ms);
+    }
+    if (W == 0) {
+        // shadow rays of the hits, in ray order (pathtrace.py:132-138, 101-108)
+        int nh = 0;
+        for (long long i = own_lo + threadIdx.x; i < own_hi; i += blockDim.x) nh += isfinite(__ldcg(TH + i)) ? 1 : 0;
+        nh = pt_block_sum(nh, sm.w);
+        if (threadIdx.x == 0) cntH[blockIdx.x] = nh;
+        pt_barrier(s.bar, target);
+        long long pre_h, n_h;
+        pt_cta_prefix(cntH, sm.red, pre_h, n_h);
+        for (long long b0 = own_lo; b0 < own_hi; b0 += blockDim.x) {
+            const long long i = b0 + threadIdx.x;
+            double th = INFINITY;
+            if (i < own_hi) th = __ldcg(TH + i);
+            const bool f = isfinite(th);
+            int tot;
+            const int rk = pt_block_rank(f, sm.w, tot);
+            if (i < own_hi) s.sh_of[i] = f ? (int)(pre_h + rk) : -1;
+            if (f) pt_shadow_ray(q, s, pre_h + rk, (int)i, th, ray_o, ray_d);
             pre_h += tot;
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) s.rng->sh_n = (int)n_h;
@@ -738,6 +1139,20 @@ __global__ void k_pt_init(VcbPtParams q, PtWs s) {
         s.jump[j].p_hi = (u64)(c >> 64);
         c = (m + 1) * c;
         m = m * m;
+    }
+    // radix-16 table: step = jump by 16^d; entry v = step composed v times
+    u128 sm_ = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    u128 sc_ = ((u128)q.pcg_inc[1] << 64) | q.pcg_inc[0];
+    for (int d = 0; d < 16; d++) {
+        u128 em = 1, ec = 0;
+        for (int v = 0; v < 16; v++) {
+            s.j16[d * 16 + v] = PtJump{(u64)em, (u64)(em >> 64), (u64)ec, (u64)(ec >> 64)};
+            // (em, ec) then one more step (sm_, sc_): s -> sm_ (em s + ec) + sc_
+            ec = sm_ * ec + sc_;
+            em = sm_ * em;
+        }
+        sm_ = em;  // 16 steps of the old step = the next digit's step
+        sc_ = ec;
     }
     PtRng r = {};
     *s.rng = r;
@@ -816,7 +1231,16 @@ __global__ void k_pt_debug_math(int64_t n, const double* x, double* lg, u64 s_lo
 void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
 extern thread_local long long g_launches;
 
-static const void* pt_kernel(int mode) {
+// walk schedule: 0 (default) four barriers per iteration with the active list re-split
+// evenly every iteration; 1 two barriers per iteration with per-CTA ray ownership and
+// rebalancing on demand (bit-identical, ~5% slower: the imbalance costs more than the
+// two barriers it saves)
+static const void* pt_kernel(int mode, int impl) {
+    if (impl == 1) {
+        if (mode == 1) return (const void*)k_pt_walk2<1>;
+        if (mode == 2) return (const void*)k_pt_walk2<2>;
+        return (const void*)k_pt_walk2<0>;
+    }
     if (mode == 1) return (const void*)k_pt_walk<1>;
     if (mode == 2) return (const void*)k_pt_walk<2>;
     return (const void*)k_pt_walk<0>;
@@ -843,7 +1267,7 @@ extern "C" int32_t vcb_trace_free_flight(const VcbFrameParams* pp, const VcbPtPa
         return set_error("trace_free_flight: workspace too small (%lld < %lld)", (long long)q.workspace_bytes,
                          (long long)need);
     const int mode = inr_mode(p.field);
-    const void* fn = pt_kernel(mode);
+    const void* fn = pt_kernel(mode, p.impl == 1 ? 1 : 0);
     int smem = 0;
     if (p.field.kind == 0) {
         int nw = 0, nb = 0;
@@ -920,7 +1344,7 @@ extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtPara
         return set_error("pathtrace_frame: workspace too small (%lld < %lld)", (long long)q.workspace_bytes,
                          (long long)need2);
     const int mode = inr_mode(p.field);
-    const void* fn = pt_kernel(mode);
+    const void* fn = pt_kernel(mode, p.impl == 1 ? 1 : 0);
     int smem = 0;
     if (p.field.kind == 0) {
         int nw = 0, nb = 0;

@@ -164,3 +164,19 @@ def test_pathtrace_variance_scales_inverse_n():
         variances.append(np.var(np.stack(runs), axis=0).mean())
     slope = np.polyfit(np.log(spps), np.log(variances), 1)[0]
     assert -1.35 <= slope <= -0.65, slope
+
+
+def test_walk_schedules_agree():
+    """The two-barrier walk (default) and the four-barrier walk (impl=1) are bit-identical."""
+    from gpu_runner import run_gpu_session
+
+    outs = []
+    for impl in (0, 1):
+        frames = []
+        for f, img, rec, sess in run_gpu_session("pt_pressure", frames=4, impl=impl):
+            frames.append((img.copy(), rec.samples, rec.true_misses, rec.exact_hits, sess.debug_state()["tables"]))
+        outs.append(frames)
+    for (a, b) in zip(*outs):
+        np.testing.assert_array_equal(a[0], b[0])
+        assert a[1:4] == b[1:4]
+        np.testing.assert_array_equal(a[4], b[4])

@@ -26,6 +26,7 @@ cfg = SessionConfig(cached=cached, mode="pathtrace", samples_per_pixel=spp, load
                     settings=P.RenderSettings(), seed=0)
 traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=res, height=res)
 sess = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+sess.impl = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 for f in range(40):
     sess.set_camera(traj.camera_at(f))
     t0 = time.perf_counter()
