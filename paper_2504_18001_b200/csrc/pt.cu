@@ -67,6 +67,7 @@ struct PtWs {
     int* list[2];
     uint8_t* flag;
     uint8_t* flag2;    // second list-flag buffer (walk rebalancing)
+    double* exitb;     // [n] cell exit of a dense ray (classify -> draw)
     float* mub;        // [n] majorant of a settled ray's cell (mu[~empty][~crossed], line 91)
     double* sh_o;      // [3n] shadow origins (primary hit points)
     double* sh_tend;   // [n] t_far of the shadow ray
@@ -98,6 +99,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
     }
     size_t o_f = take((size_t)n);
     size_t o_f2 = take((size_t)n);
+    size_t o_ex = take((size_t)n * 8);
     size_t o_mub = take((size_t)n * 4);
     size_t o_sho = take((size_t)n * 24);
     size_t o_sht = take((size_t)n * 8);
@@ -121,6 +123,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
         }
         s->flag = (uint8_t*)(p + o_f);
         s->flag2 = (uint8_t*)(p + o_f2);
+        s->exitb = (double*)(p + o_ex);
         s->mub = (float*)(p + o_mub);
         s->sh_o = (double*)(p + o_sho);
         s->sh_tend = (double*)(p + o_sht);
@@ -395,6 +398,8 @@ struct PtWalk {
     double oc[3], dc[3], t0c;
     int o_stride, d_stride, t0_stride;
     int which;        // 0 primary, 1 shadow
+    int mu_smem;      // majorant grid staged in shared memory after the MLP weights
+    int mu_off;       // its float offset in the dynamic shared memory
 };
 
 struct PtGeo {
@@ -405,7 +410,8 @@ struct PtGeo {
 
 // pathtrace.py:54-68 for one ray
 __device__ __forceinline__ PtGeo pt_geo(const VcbFrameParams& p, float dens_f, double ox, double oy, double oz,
-                                        double dx, double dy, double dz, double t, double tend) {
+                                        double dx, double dy, double dz, double t, double tend,
+                                        const float* mu_grid = nullptr) {
     PtGeo g;
     const double px = DADD(ox, DMUL(dx, t)), py = DADD(oy, DMUL(dy, t)), pz = DADD(oz, DMUL(dz, t));
     const double lo = -1e-12, hi = 1.000000000001;
@@ -420,7 +426,8 @@ __device__ __forceinline__ PtGeo pt_geo(const VcbFrameParams& p, float dens_f, d
     cx = cx < 0 ? 0 : (cx > p.adv.gx - 1 ? p.adv.gx - 1 : cx);
     cy = cy < 0 ? 0 : (cy > p.adv.gy - 1 ? p.adv.gy - 1 : cy);
     cz = cz < 0 ? 0 : (cz > p.adv.gz - 1 ? p.adv.gz - 1 : cz);
-    g.mu = FMUL(__ldg(p.mu + (cz * p.adv.gy + cy) * p.adv.gx + cx), dens_f);
+    const long long cell = (cz * p.adv.gy + cy) * p.adv.gx + cx;
+    g.mu = FMUL(mu_grid ? mu_grid[cell] : __ldg(p.mu + cell), dens_f);
     // _cell_exit (21-25)
     const double bx = DMUL((double)(cx + (dx > 0.0 ? 1 : 0)), p.adv.cwx);
     const double by = DMUL((double)(cy + (dy > 0.0 ? 1 : 0)), p.adv.cwy);
@@ -534,6 +541,13 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     extern __shared__ __align__(16) float smem[];
     MlpSmem mlp;
     if (kInr != 0) stage_mlp(p.field, smem, mlp);
+    const float* MUG = nullptr;  // majorant grid in shared memory when it fits
+    if (wk.mu_smem) {
+        float* g = smem + wk.mu_off;
+        const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+        for (long long c = threadIdx.x; c < cells; c += blockDim.x) g[c] = __ldg(p.mu + c);
+        MUG = g;
+    }
     for (int i = threadIdx.x; i < q.n_tf * 5; i += blockDim.x) sm.tf[i] = q.tf[i];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.j16[i] = s.j16[i];
     unsigned target = 0;
@@ -620,7 +634,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                 ray_o(r, ox, oy, oz);
                 ray_d(r, dx, dy, dz);
                 const double t = __ldcg(T + r), te = __ldcg(wk.tend + r);
-                const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te);
+                const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te, MUG);
                 uint8_t cls = 0;
                 if (!g.outside) {
                     if (g.mu <= 0.0f) {
@@ -629,7 +643,10 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                             cls = 1;
                         }
                     } else {
-                        cls = 2;
+                        // dense: keep mu, the cell exit and at_end for the draw phase
+                        __stcg(s.mub + i, g.mu);
+                        __stcg(s.exitb + i, g.exit_t);
+                        cls = g.at_end ? 4 : 2;
                         cnt++;
                     }
                 }
@@ -654,26 +671,24 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                     cls = __ldcg(s.flag + i);
                     r = __ldcg(in + i);
                 }
+                const bool dense = cls == 2 || cls == 4;
                 int tot;
-                const int rk = pt_block_rank(cls == 2, sm.w, tot);
-                if (cls == 2) {
-                    double ox, oy, oz, dx, dy, dz;
-                    ray_o(r, ox, oy, oz);
-                    ray_d(r, dx, dy, dz);
-                    const double t = __ldcg(T + r), te = __ldcg(wk.tend + r);
-                    const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te);
+                const int rk = pt_block_rank(dense, sm.w, tot);
+                if (dense) {
+                    const double t = __ldcg(T + r);
+                    const float mu = __ldcg(s.mub + i);
+                    const double exit_t = __ldcg(s.exitb + i);
                     const double xi = pcg_out(pcg_jump16(Sr, (u64)rk + 1, sm.j16));
-                    const double tc = DSUB(t, __ddiv_rn(pt_log1p(-xi), (double)g.mu));
-                    if (tc >= g.exit_t) {
-                        if (g.at_end) {
+                    const double tc = DSUB(t, __ddiv_rn(pt_log1p(-xi), (double)mu));
+                    if (tc >= exit_t) {
+                        if (cls == 4) {
                             cls = 0;
                         } else {
-                            __stcg(T + r, DADD(g.exit_t, 1e-9));
+                            __stcg(T + r, DADD(exit_t, 1e-9));
                             cls = 1;
                         }
                     } else {
                         __stcg(T + r, tc);
-                        __stcg(s.mub + i, g.mu);
                         cls = 3;
                         cnt++;
                     }
@@ -1354,6 +1369,10 @@ extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtPara
         }
         smem = (nw + nb) * 4;
     }
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    const int mu_off = (smem / 4 + 3) & ~3;
+    const bool mu_smem = p.impl != 1 && (long long)mu_off * 4 + cells * 4 <= 200 * 1024;
+    if (mu_smem) smem = mu_off * 4 + (int)cells * 4;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPtThreads, smem);
@@ -1379,6 +1398,8 @@ extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtPara
     prim.t0_stride = 1;
     prim.tend = w.ray_tex;
     prim.which = 0;
+    prim.mu_smem = mu_smem ? 1 : 0;
+    prim.mu_off = mu_off;
     PtWalk shad = {};
     shad.n_dev = &s.rng->sh_n;
     shad.o = s.sh_o;
@@ -1389,6 +1410,8 @@ extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtPara
     shad.t0_stride = 0;
     shad.tend = s.sh_tend;
     shad.which = 1;
+    shad.mu_smem = mu_smem ? 1 : 0;
+    shad.mu_off = mu_off;
     VcbFrameParams pc = p;
     VcbPtParams qc = q;
     FrameWs wc = w;
