@@ -219,7 +219,9 @@ typedef struct {
                                 are updated in place */
     VcbField target;         /* the field fitted (lattice / procedural / INR) */
     int64_t batch, steps, step0;   /* step0 = optimizer steps already taken (Adam t) */
-    int32_t optimizer, pad_;       /* 0 = Adam (train.py:51-75), 1 = SGD (40-48) */
+    int32_t optimizer;             /* 0 = Adam (train.py:51-75), 1 = SGD (40-48), 2 = none (lr 0) */
+    int32_t flags;                 /* bit 0: pos/targets given by the caller (no PCG batch, no decode);
+                                      bit 1: keep the gradients (loss_and_grads, train.py:16-37: no update) */
     double lr, beta1, beta2, eps, clip_norm;   /* clip_norm <= 0: no clipping (78-85) */
     uint64_t pcg_state[2], pcg_inc[2];
     uint64_t draw0;

@@ -103,7 +103,7 @@ class VcbPtParams(C.Structure):
 
 class VcbTrainParams(C.Structure):
     _fields_ = [("model", VcbField), ("target", VcbField), ("batch", i64), ("steps", i64), ("step0", i64),
-                ("optimizer", i32), ("pad_", i32), ("lr", f64), ("beta1", f64), ("beta2", f64), ("eps", f64),
+                ("optimizer", i32), ("flags", i32), ("lr", f64), ("beta1", f64), ("beta2", f64), ("eps", f64),
                 ("clip_norm", f64), ("pcg_state", C.c_uint64 * 2), ("pcg_inc", C.c_uint64 * 2),
                 ("draw0", C.c_uint64), ("n_table_params", i64), ("n_weights", i64), ("n_params", i64),
                 ("grads", vp), ("m", vp), ("v", vp), ("pos", vp), ("targets", vp), ("loss", vp), ("scratch", vp),

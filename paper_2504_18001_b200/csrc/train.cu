@@ -349,11 +349,17 @@ extern "C" int32_t vcb_train_steps(const VcbTrainParams* pp, void* stream_) {
     const int gu = grid_for(P.n_params, 256);
     long long launches = 1;
     for (long long s = 0; s < P.steps; s++) {
-        k_tr_positions<<<gp, 256, 0, st>>>(P, s);
-        int32_t rc = vcb_field_points(&P.target, P.batch, P.pos, P.targets, P.nonfinite, st);
-        if (rc != 0) return rc;
+        if (!(P.flags & 1)) {
+            k_tr_positions<<<gp, 256, 0, st>>>(P, s);
+            int32_t rc = vcb_field_points(&P.target, P.batch, P.pos, P.targets, P.nonfinite, st);
+            if (rc != 0) return rc;
+        }
         if (P.model.out_sigmoid) k_tr_step<true><<<gs, kTrB, smem, st>>>(P, s);
         else k_tr_step<false><<<gs, kTrB, smem, st>>>(P, s);
+        if (P.flags & 2) {
+            launches += 1;
+            continue;  // loss_and_grads: gradients stay in P.grads
+        }
         if (P.clip_norm > 0.0) k_tr_gnorm<<<gu, 256, 0, st>>>(P);
         const double t = (double)(P.step0 + s + 1);
         const double bc1 = 1.0 - std::pow(P.beta1, t), bc2 = 1.0 - std::pow(P.beta2, t);

@@ -102,6 +102,55 @@ def train(model, field_src, steps: int, batch_size: int = DEFAULT_BATCH_SIZE, le
     return TrainResult(model, trace)
 
 
+def loss_and_grads(model, positions, targets, device=None):
+    """train.py:16-37 on the GPU: MSE loss and the gradient of every parameter, in
+    model.parameters() order (tables, weights, biases) and the model's dtype."""
+    g, mc = model.grid_config, model.mlp_config
+    if (g.levels, g.features_per_entry, mc.hidden_width, mc.hidden_layers) != (8, 2, 32, 2):
+        raise ConfigError("the GPU trainer supports the default 8x2 hash grid + 16-32-32-1 MLP")
+    dev = require_cuda(device)
+    pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+    tg = np.ascontiguousarray(np.asarray(targets, dtype=np.float32).reshape(-1))
+    B = pos.shape[0]
+    if tg.shape[0] != B:
+        raise ValueError("positions and targets differ in length")
+    df = _inr_desc(model, dev, clip=False)
+    tab, wt, bt = df._keep
+    n_tab, n_w, n_b = tab.numel(), wt.numel(), bt.numel()
+    n_p = n_tab + n_w + n_b
+    f64 = dict(dtype=torch.float64, device=dev)
+    grads = torch.zeros(n_p, **f64)
+    dpos = torch.from_numpy(pos).to(dev)
+    dtg = torch.from_numpy(tg).to(dev)
+    loss = torch.zeros(1, **f64)
+    scratch = torch.zeros(8, **f64)
+    nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
+    jump = torch.empty(int(N.load().vcb_train_workspace_bytes(B)), dtype=torch.uint8, device=dev)
+    p = N.VcbTrainParams()
+    p.model = df.desc
+    p.batch, p.steps, p.step0 = B, 1, 0
+    p.optimizer, p.flags = 2, 3
+    p.n_table_params, p.n_weights, p.n_params = n_tab, n_w, n_p
+    p.grads, p.m, p.v = ptr(grads), ptr(grads), ptr(grads)
+    p.pos, p.targets, p.loss, p.scratch, p.nonfinite, p.jump = (ptr(dpos), ptr(dtg), ptr(loss), ptr(scratch),
+                                                                 ptr(nonfinite), ptr(jump))
+    stream = torch.cuda.current_stream(dev)
+    N.call("vcb_train_steps", C.byref(p), C.c_void_p(stream.cuda_stream))
+    stream.synchronize()
+    gh = grads.cpu().numpy().astype(model.dtype)
+    out, o = [], 0
+    for t in model.tables:
+        out.append(gh[o:o + t.size].reshape(t.shape))
+        o += t.size
+    for w in model.weights:
+        out.append(gh[o:o + w.size].reshape(w.shape))
+        o += w.size
+    for b in model.biases:
+        out.append(gh[o:o + b.size].reshape(b.shape))
+        o += b.size
+    return float(loss.item()) / B, out
+
+
 def psnr_on_lattice(model, field_src, dims=None) -> float:
     """train.py:135-143: reconstruction PSNR against the field's lattice, in dB."""
     dims = dims or field_src.domain.dims

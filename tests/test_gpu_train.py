@@ -99,3 +99,58 @@ def test_training_reduces_loss_at_scale():
     res = train(model, field, steps=100, seed=7)
     assert res.final_loss < 0.5 * res.loss_trace[0]
     assert psnr_on_lattice(res.model, field) > p0 + 3.0
+
+
+def test_loss_and_grads_matches_reference():
+    """train.py:16-37 on one batch: the reference's loss and every parameter gradient."""
+    from conftest import load_golden
+    from paper_2504_18001_b200.train import loss_and_grads
+
+    g = load_golden("train.npz")
+    model, _ = _setup()
+    loss, grads = loss_and_grads(model, g["lg_pos"], g["lg_targets"])
+    assert abs(loss - float(g["lg_loss"])) <= 1e-6 * float(g["lg_loss"])
+    nt = len(model.tables)
+    for i, gr in enumerate(grads):
+        assert gr.dtype == np.float32 and gr.shape == model.parameters()[i].shape
+        if i < nt:
+            np.testing.assert_allclose(gr[g[f"lg_g{i}_rows"]], g[f"lg_g{i}"], rtol=1e-4, atol=1e-9)
+            assert abs(float(np.abs(gr).sum(dtype=np.float64)) - float(g[f"lg_g{i}_sum"])) <= 1e-4 * float(
+                g[f"lg_g{i}_sum"]) + 1e-9
+        else:
+            want = g[f"lg_g{i}"]
+            np.testing.assert_allclose(gr, want, rtol=1e-4, atol=1e-6 * float(np.abs(want).max()))
+
+
+def test_loss_and_grads_finite_differences():
+    """test_inr.py:139-160's check in f32 on the default network (randomised weights so the
+    ReLUs are not all at their kinks): central differences of the GPU loss against the GPU
+    gradient at the largest-gradient entry of every parameter array."""
+    from gpu_runner import product_inr
+    from paper_2504_18001_b200.train import loss_and_grads
+
+    model = product_inr((32, 32, 32))
+    rng = np.random.default_rng(0)
+    pos = rng.random((256, 3))
+    targets = rng.random(256).astype(np.float32)
+    _, grads = loss_and_grads(model, pos, targets)
+    eps = 1e-3
+    worst = 0.0
+    params = model.parameters()
+    for i, gr in enumerate(grads):
+        k = int(np.argmax(np.abs(gr).reshape(-1)))
+        flat = params[i].reshape(-1)
+        orig = flat[k]
+        flat[k] = orig + eps
+        model.set_parameters(params)
+        lp, _ = loss_and_grads(model, pos, targets)
+        flat[k] = orig - eps
+        model.set_parameters(params)
+        lm, _ = loss_and_grads(model, pos, targets)
+        flat[k] = orig
+        model.set_parameters(params)
+        fd = (lp - lm) / (2 * eps)
+        gv = float(gr.reshape(-1)[k])
+        print("fd check", i, k, fd, gv)
+        worst = max(worst, abs(fd - gv) / max(abs(fd), abs(gv), 1e-6))
+    assert worst <= 2e-2, worst
