@@ -223,7 +223,7 @@ class DeviceCache:
         self.staging = torch.zeros(mr * b3, dtype=torch.float32, device=device)
         self.staged_keys = t(mr, torch.int64, -1)
         wsb = N.load().vcb_maint_workspace_bytes(lay.total, self.slots, mr)
-        self.workspace = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.workspace = torch.zeros(wsb, dtype=torch.uint8, device=device)
         self.dbg_reports = t(2 * lay.total, torch.int64, 0) if debug else None
         self.frame = 0  # Mrpd.frame: the probe stamp clock (P11)
         max_lin = max(counts) - 1

@@ -400,6 +400,9 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     int64_t need = maint_ws_layout(P.total, P.workspace, &w);
     if (need > P.workspace_bytes) return set_error("maintenance: workspace too small");
     cudaMemsetAsync(w.ctr, 0, 64, st);
+    // the decode flag is per maintenance (set by this call's decode, read by k_post_decode);
+    // the workspace comes uninitialised from the caller
+    cudaMemsetAsync(w.nonfinite, 0, 4, st);
     const int g = grid_for(P.total, 256, 8);
     // 1. drain miss reports into the request table (session.py:135-136)
     k_report<<<g, 256, 0, st>>>(P, w);

@@ -494,9 +494,10 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
         if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768, 0);
         if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640, 0);
-        if (p.impl == 8) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 1);
+        if (p.impl == 8) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 1);
+        if (p.impl == 9) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
         if (p.impl == 7) return launch_wave4_frame(p, st, &g_launches, ev, &g_ev_used);
-        return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
+        return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;

@@ -747,13 +747,16 @@ __global__ void __launch_bounds__(NT, 1)
 static const void* wave3_kernel(int mode, int nt) {
     if (nt == 768) return mode == 1 ? (const void*)k_wave3_march<1, 768> : (const void*)k_wave3_march<0, 768>;
     if (nt == 640) return mode == 1 ? (const void*)k_wave3_march<1, 640> : (const void*)k_wave3_march<0, 640>;
+    if (nt == 384) return mode == 1 ? (const void*)k_wave3_march<1, 384> : (const void*)k_wave3_march<0, 384>;
     return mode == 1 ? (const void*)k_wave3_march<1, 512>
                      : mode == 2 ? (const void*)k_wave3_march<2, 512> : (const void*)k_wave3_march<0, 512>;
 }
 
 void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
 
-// nt: threads per CTA (768 = 24 warps at <= 80 registers, 512 = 16 warps at <= 128)
+// nt: threads per CTA (384 = 12 warps at <= 168 registers, the default: the 512-thread
+// build spills ~300 B per thread at 128 registers and is 11% slower; 768 = 24 warps at
+// <= 80 registers)
 int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
                        int nt, int mu_mode) {
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
