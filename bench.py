@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--uncached-steps", type=int, default=5, help="frames of the no-cache INR baseline (0 = skip)")
+    ap.add_argument("--train-steps", type=int, default=50,
+                    help="INR training steps at batch 65536 (inr/train.py on the GPU; 0 = skip)")
     ap.add_argument("--pt-steps", type=int, default=5,
                     help="frames of the path-trace mode (pathtrace.py, spp 1) cached and uncached (0 = skip)")
     ap.add_argument("--mp", default="auto", choices=["auto", "frames", "tiles"],
@@ -479,6 +481,30 @@ def main():
             del psess
         pathtrace["cache_speedup"] = pathtrace["cached"]["fps"] / pathtrace["uncached"]["fps"]
 
+    # ---- INR training (inr/train.py): Adam steps at the reference's
+    # default batch on a 64^3 lattice target, device-timed
+    training = None
+    if ctx.world == 1 and args.train_steps > 0:
+        from paper_2504_18001_b200.train import psnr_on_lattice, train
+
+        lat = np.random.default_rng(9).random((64, 64, 64)).astype(np.float32)
+        tfield = P.RawLatticeField(lat, P.FieldDomain((64, 64, 64)))
+        tmodel = P.InrModel(P.HashGridConfig(), P.MLPConfig(), P.FieldDomain((64, 64, 64)), seed=0)
+        train(tmodel, tfield, steps=3, seed=1)  # warm-up (module load, allocations)
+        tmodel = P.InrModel(P.HashGridConfig(), P.MLPConfig(), P.FieldDomain((64, 64, 64)), seed=0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        tres = train(tmodel, tfield, steps=args.train_steps, seed=2)
+        e1.record()
+        torch.cuda.synchronize()
+        tms = e0.elapsed_time(e1) / args.train_steps
+        training = {"ms_per_step": tms, "batch": 65536, "samples_per_s": 65536 / (tms / 1000.0),
+                    "steps": args.train_steps, "loss_first_last": [float(tres.loss_trace[0]), tres.final_loss],
+                    "note": "train(model, field, steps, batch_size=65536, adam lr 1e-2): PCG64 batch, target decode, "
+                            "fused forward/backward + f64 scatter-add, Adam; timed on the current stream incl. the "
+                            "host round trip of the loss trace"}
+
     decode = None
     if ctx.rank == 0 and args.decode_n > 0:
         try:
@@ -509,7 +535,7 @@ def main():
                          "march_share_of_step": (march_ms / ctx.world) / total_ms if total_ms else None,
                          "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "inr_decode": decode, "uncached_inr_baseline": uncached,
-            "pathtrace": pathtrace,
+            "pathtrace": pathtrace, "inr_training": training,
             "clocks": clk.summary(), "gpu_launches": launches,
             "samples_per_frame": samples_all / (args.steps * per_step),
             "inr_samples_per_frame": float(np.mean([r.true_misses for r in recs])) + 40 * 16 ** 3,
