@@ -7,8 +7,8 @@ device memory and streams.  There is no CPU fallback.
 """
 
 from .cache import BrickKey, BrickLayout, CacheConfig, PoolSpec
-from .errors import (ConfigError, DomainError, IngestionError, ModelCorruptError, RenderError, VoxcacheError,
-                     WeightFormatError)
+from .errors import (ConfigError, DomainError, IngestionError, ModelCorruptError, RenderError,
+                     TrainingDivergedError, VoxcacheError, WeightFormatError)
 from .fields import Field, FieldDomain, ProceduralField, RawLatticeField, make_procedural
 from .inr import HashGridConfig, InrField, InrModel, MLPConfig
 from .render import Camera, RenderSettings, TransferFunction, grayscale_ramp, transparent, warm_body
@@ -29,4 +29,11 @@ def __getattr__(name):
         from . import harness
 
         return getattr(harness, name)
+    # voxcache.inr's training API (the function itself is paper_2504_18001_b200.train.train,
+    # like voxcache.inr.train.train: the submodule owns the package attribute `train`)
+    if name in ("loss_and_grads", "psnr_on_lattice", "TrainResult"):
+        import importlib
+
+        mod = importlib.import_module(".train", __name__)
+        return getattr(mod, name)
     raise AttributeError(name)
