@@ -11,16 +11,18 @@
 // and a final pass writing total / spp and hits / spp (143-146).
 //
 // A walk is one persistent cooperative kernel (one 512-thread CTA per SM) that
-// runs the reference's wavefront iterations with four grid barriers each:
+// runs the reference's wavefront iterations with three grid barriers each:
 //   1 classify: position, outside test, macro cell, majorant, cell exit; empty
-//     cells hop or escape; the rest draw a free flight
+//     cells hop or escape; the rest draw a free flight (done by the previous
+//     iteration's compaction for every survivor, so only iteration 0 has its own pass)
 //   2 draws: dense rays ranked in ray order take numpy PCG64 draw D + rank
 //     (rng.random(dense.size), line 79), free flight t - log1p(-xi)/mu
 //   3 sample: settled rays ranked in ray order are one VolumeSampler.sample batch
 //     (XorShift32 lane = rank, with the reference's lane-pool reseeding,
 //     sampler.py:206-213), MRPD probe + miss filing + true-miss INR, then the
 //     acceptance draw D + n_dense + rank (line 91)
-//   4 ordered compaction of the rays still walking.
+//   4 ordered compaction of the rays still walking, fused with their classification
+//     for the next iteration (dense counts land on the CTA owning the new slot).
 // Ranks come from per-CTA counts (each CTA owns a contiguous chunk of the active
 // list) plus a block scan, so every draw index, lane and list position equals the
 // reference's.  The PCG64 state of draw D is a jump of the seeded state by D + 1
@@ -623,10 +625,13 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     for (; k < q.max_walk && m > 0; k++) {
         const int* in = s.list[k & 1];
         int* out = s.list[(k + 1) & 1];
-        pt_barrier(s.bar, target);  // list k complete; counts of the previous round consumed
+        uint8_t* FLc = (k & 1) ? s.flag2 : s.flag;  // flags of list k / list k+1
+        uint8_t* FLn = (k & 1) ? s.flag : s.flag2;
+        pt_barrier(s.bar, target);  // list k, its flags and dense counts complete
         pt_chunk(m, lo, hi);
-        // phase 1: classify (54-75)
-        {
+        // phase 1: classify (54-75); from iteration 1 on the compaction of the previous
+        // iteration has classified every survivor already
+        if (k == 0) {
             int cnt = 0;
             for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
                 const int r = __ldcg(in + i);
@@ -650,13 +655,15 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                         cnt++;
                     }
                 }
-                __stcg(s.flag + i, cls);
+                __stcg(FLc + i, cls);
             }
             cnt = warp_sum(cnt);
             if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(cnt1 + blockIdx.x, cnt);
             if (threadIdx.x == 0) cnt0[blockIdx.x] = 0;
+            pt_barrier(s.bar, target);
+        } else if (threadIdx.x == 0) {
+            cnt0[blockIdx.x] = 0;  // survivor counts of iteration k-1 were consumed before the barrier
         }
-        pt_barrier(s.bar, target);
         long long pre_d, n_dense;
         pt_cta_prefix(cnt1, sm.red, pre_d, n_dense);
         // phase 2: free-flight draws of the dense rays (77-88)
@@ -668,7 +675,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                 uint8_t cls = 0;
                 int r = 0;
                 if (i < hi) {
-                    cls = __ldcg(s.flag + i);
+                    cls = __ldcg(FLc + i);
                     r = __ldcg(in + i);
                 }
                 const bool dense = cls == 2 || cls == 4;
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                         cls = 3;
                         cnt++;
                     }
-                    __stcg(s.flag + i, cls);
+                    __stcg(FLc + i, cls);
                 }
                 pre_d += tot;
             Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
@@ -728,7 +735,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                 uint8_t cls = 0;
                 int r = 0;
                 if (i < hi) {
-                    cls = __ldcg(s.flag + i);
+                    cls = __ldcg(FLc + i);
                     r = __ldcg(in + i);
                 }
                 int tot;
@@ -754,7 +761,7 @@ __global__ void __launch_bounds__(kPtThreads, 1)
                     }
                 }
                 if (cls == 1) cls = __ldcg(T + r) < __ldcg(wk.tend + r) ? 1 : 0;  // walking &= t < t_end
-                if (i < hi) __stcg(s.flag + i, cls);
+                if (i < hi) __stcg(FLc + i, cls);
                 cnt += cls;
                 pre_s += tot;
                 Sr = pcg_jump16(Sr, (u64)tot, sm.j16);
@@ -768,14 +775,41 @@ __global__ void __launch_bounds__(kPtThreads, 1)
         long long pre_v, m_next;
         pt_cta_prefix(cnt0, sm.red, pre_v, m_next);
         if (threadIdx.x == 0) cnt2[blockIdx.x] = 0;
-        // phase 4: ordered compaction of the walking rays
+        // phase 4: ordered compaction of the walking rays, fused with their classification
+        // for iteration k+1 (a ray retired by it keeps its slot with flag 0 and leaves at the
+        // next compaction); dense counts go to the CTA that owns the slot in iteration k+1
+        const long long ch_next = (m_next + gridDim.x - 1) / gridDim.x;
         for (long long b0 = lo; b0 < hi; b0 += blockDim.x) {
             const long long i = b0 + threadIdx.x;
             bool f = false;
-            if (i < hi) f = __ldcg(s.flag + i) != 0;
+            if (i < hi) f = __ldcg(FLc + i) != 0;
             int tot;
             const int rk = pt_block_rank(f, sm.w, tot);
-            if (f) __stcg(out + pre_v + rk, __ldcg(in + i));
+            if (f) {
+                const long long dst = pre_v + rk;
+                const int r = __ldcg(in + i);
+                __stcg(out + dst, r);
+                double ox, oy, oz, dx, dy, dz;
+                ray_o(r, ox, oy, oz);
+                ray_d(r, dx, dy, dz);
+                const double t = __ldcg(T + r), te = __ldcg(wk.tend + r);
+                const PtGeo g = pt_geo(p, dens_f, ox, oy, oz, dx, dy, dz, t, te, MUG);
+                uint8_t cls = 0;
+                if (!g.outside) {
+                    if (g.mu <= 0.0f) {
+                        if (!g.at_end) {
+                            __stcg(T + r, DADD(g.exit_t, 1e-9));
+                            cls = 1;
+                        }
+                    } else {
+                        __stcg(s.mub + dst, g.mu);
+                        __stcg(s.exitb + dst, g.exit_t);
+                        cls = g.at_end ? 4 : 2;
+                        warp_aggregated_add(cnt1, dst / ch_next);
+                    }
+                }
+                __stcg(FLn + dst, cls);
+            }
             pre_v += tot;
         }
         m = m_next;
@@ -796,17 +830,17 @@ __global__ void __launch_bounds__(kPtThreads, 1)
     if (W == 0) {
         // shadow rays of the hits, in ray order (pathtrace.py:132-138, 101-108)
         pt_barrier(s.bar, target);
-        if (threadIdx.x == 0) cnt0[blockIdx.x] = 0;
         pt_chunk(n, lo, hi);
         {
+            // cnt2 is zero here: reset after the last iteration's third barrier, unused since
             int cnt = 0;
             for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) cnt += isfinite(__ldcg(TH + i)) ? 1 : 0;
             cnt = warp_sum(cnt);
-            if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(cnt1 + blockIdx.x, cnt);
+            if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(cnt2 + blockIdx.x, cnt);
         }
         pt_barrier(s.bar, target);
         long long pre_h, n_h;
-        pt_cta_prefix(cnt1, sm.red, pre_h, n_h);
+        pt_cta_prefix(cnt2, sm.red, pre_h, n_h);
         for (long long b0 = lo; b0 < hi; b0 += blockDim.x) {
             const long long i = b0 + threadIdx.x;
             double th = INFINITY;
@@ -1246,7 +1280,7 @@ __global__ void k_pt_debug_math(int64_t n, const double* x, double* lg, u64 s_lo
 void launch_rays(const VcbFrameParams& p, const FrameWs& w, cudaStream_t st);
 extern thread_local long long g_launches;
 
-// walk schedule: 0 (default) four barriers per iteration with the active list re-split
+// walk schedule: 0 (default) three barriers per iteration with the active list re-split
 // evenly every iteration; 1 two barriers per iteration with per-CTA ray ownership and
 // rebalancing on demand (bit-identical, ~5% slower: the imbalance costs more than the
 // two barriers it saves)
