@@ -319,6 +319,10 @@ class RenderSession:
             self._stats.zero_()
             p = self._frame_params(img)
             if self.mode == "pathtrace":
+                if self.band != (0, 1):
+                    # one PCG64 stream orders the whole bundle (pathtrace.py:117-131): a band
+                    # would draw different numbers than the full frame
+                    raise ConfigError("path tracing renders whole frames; use alternate-frame rendering")
                 q = self._pt_params(p)
                 N.call("vcb_pathtrace_frame", C.byref(p), C.byref(q), stream_ptr(self.stream))
             else:
