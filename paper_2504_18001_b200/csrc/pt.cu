@@ -53,7 +53,7 @@ struct PtRng {
     u64 draws;        // numpy PCG64 draws consumed this frame
     long long pool;   // XorShift32 lanes seeded this frame (0 = not yet, sampler.py:206)
     long long salt;   // _reseed_salt
-    unsigned gen;     // lane generation (lanes seeded lazily: lane_gen != gen -> reseed)
+    unsigned gen;     // lane generation (lanes seeded lazily: stored generation != gen -> reseed)
     unsigned pad;
     u64 base;         // splitmix64(seed ^ frame' * GOLDEN) of generation gen
     long long iters;  // walk iterations (stats)
@@ -76,8 +76,7 @@ struct PtWs {
     int* sh_of;        // [n] primary ray -> shadow ray (-1 = no hit)
     double* total;     // [3n]
     double* hits;      // [n]
-    uint32_t* lane_st;
-    uint32_t* lane_gen;
+    unsigned long long* lane;  // [n] XorShift32 lane: (generation << 32) | state
     int* cnt;          // [4][kPtMaxCtas]
     unsigned* bar;
     PtRng* rng;
@@ -108,8 +107,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
     size_t o_shof = take((size_t)n * 4);
     size_t o_tot = take((size_t)n * 24);
     size_t o_hit = take((size_t)n * 8);
-    size_t o_ls = take((size_t)n * 4);
-    size_t o_lg = take((size_t)n * 4);
+    size_t o_ls = take((size_t)n * 8);
     size_t o_cnt = take((size_t)4 * kPtMaxCtas * 4);
     size_t o_bar = take(64);
     size_t o_rng = take(sizeof(PtRng));
@@ -132,8 +130,7 @@ inline int64_t pt_ws_layout(int64_t n, void* base, PtWs* s) {
         s->sh_of = (int*)(p + o_shof);
         s->total = (double*)(p + o_tot);
         s->hits = (double*)(p + o_hit);
-        s->lane_st = (uint32_t*)(p + o_ls);
-        s->lane_gen = (uint32_t*)(p + o_lg);
+        s->lane = (unsigned long long*)(p + o_ls);
         s->cnt = (int*)(p + o_cnt);
         s->bar = (unsigned*)(p + o_bar);
         s->rng = (PtRng*)(p + o_rng);
@@ -460,10 +457,10 @@ __device__ __forceinline__ float pt_sample(const VcbFrameParams& p, const PtWs& 
     if (p.cached) {
         double u = 0.0;
         if (p.probe.mode != 2) {
-            uint32_t st = (__ldcg(s.lane_gen + lane) == R.gen) ? __ldcg(s.lane_st + lane) : lane_seed(R.base, (u64)lane);
+            const unsigned long long w = __ldcg(s.lane + lane);
+            uint32_t st = ((unsigned)(w >> 32) == R.gen) ? (uint32_t)w : lane_seed(R.base, (u64)lane);
             st = xorshift32(st);
-            __stcg(s.lane_st + lane, st);
-            __stcg(s.lane_gen + lane, R.gen);
+            __stcg(s.lane + lane, ((unsigned long long)R.gen << 32) | st);
             u = DMUL((double)st, 2.3283064365386963e-10);
         }
         const double ex = DSUB(px, p.cam.origin[0]), ey = DSUB(py, p.cam.origin[1]), ez = DSUB(pz, p.cam.origin[2]);
@@ -1329,7 +1326,7 @@ extern "C" int32_t vcb_trace_free_flight(const VcbFrameParams* pp, const VcbPtPa
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int G = device_sms();
     if (G > kPtMaxCtas) G = kPtMaxCtas;
-    if (n > 0) cudaMemsetAsync(s.lane_gen, 0xFF, (size_t)n * 4, st);
+    if (n > 0) cudaMemsetAsync(s.lane, 0xFF, (size_t)n * 8, st);
     cudaMemsetAsync(s.cnt, 0, (size_t)4 * kPtMaxCtas * 4, st);
     cudaMemsetAsync(s.bar, 0, 64, st);
     k_pt_init<<<1, 32, 0, st>>>(q, s);
@@ -1415,7 +1412,7 @@ extern "C" int32_t vcb_pathtrace_frame(const VcbFrameParams* pp, const VcbPtPara
     if (G > kPtMaxCtas) G = kPtMaxCtas;
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     cudaMemsetAsync(w.ctr_iter, 0, w.ctr_iter_bytes, st);
-    cudaMemsetAsync(s.lane_gen, 0xFF, (size_t)npix * 4, st);
+    cudaMemsetAsync(s.lane, 0xFF, (size_t)npix * 8, st);
     cudaMemsetAsync(s.total, 0, (size_t)npix * 24, st);
     cudaMemsetAsync(s.hits, 0, (size_t)npix * 8, st);
     cudaMemsetAsync(s.cnt, 0, (size_t)4 * kPtMaxCtas * 4, st);
