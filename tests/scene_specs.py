@@ -111,4 +111,10 @@ SESSION_SPECS = {
         brick=16, pool=(2, 2, 2), policy=dict(lod_scale=1.2, preload_frames=20),
         settings=dict(pt_density=40.0), res=(32, 32), frames=2, cam_step=30,
     ),
+    # anisotropic dims, non-power-of-two brick, LoD mode off, spp 3, seed 2
+    "pt_aniso": dict(
+        field="lattice", field_seed=3, dims=(40, 48, 56), tf=("warm_body", 0.4, 0.9), mode="pathtrace", spp=3,
+        brick=10, pool=(3, 3, 3), policy=dict(lod_scale=2.0, preload_frames=3, mode="off"),
+        settings=dict(pt_density=35.0, pt_ambient=0.35), res=(40, 32), frames=6, cam_step=9, radius=1.9, seed=2,
+    ),
 }

@@ -66,7 +66,7 @@ def test_operator_passes_bit_exact_vs_reference(name):
 
 
 EXACT = ["lattice64", "lattice64_paged", "lattice64_fifo", "aniso_b10", "events", "pressure", "pressure_fifo",
-         "pt_lattice64", "pt_pressure"]
+         "pt_lattice64", "pt_pressure", "pt_aniso"]
 
 
 @pytest.mark.parametrize("name", EXACT)
