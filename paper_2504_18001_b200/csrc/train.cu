@@ -25,8 +25,8 @@ namespace cinr {
 
 typedef unsigned __int128 u128;
 
-constexpr int kTrB = 128;   // samples per CTA
-constexpr int kTrS = 33;    // padded row stride (floats) of the per-sample smem rows
+constexpr int kTrB = 96;    // samples per CTA (5 CTAs = 15 warps per SM at <= 136 registers)
+constexpr int kTrS = kTrB + 1;  // padded column stride: activations are stored feature-major
 
 struct TrJump {
     u64 m_lo, m_hi, p_lo, p_hi;
@@ -79,18 +79,17 @@ __global__ void k_tr_positions(VcbTrainParams P, long long step) {
 }
 
 struct TrSmem {
-    float feat[kTrB][17];
-    float h0[kTrB][kTrS];
-    float h1[kTrB][kTrS];
-    float d1[kTrB][kTrS];
-    float d2[kTrB][kTrS];
+    float feat[16][kTrS];  // [feature][sample]; d2 is recomputed from delta, h1 and W2
+    float h0[32][kTrS];
+    float h1[32][kTrS];
+    float d1[32][kTrS];
     float delta[kTrB];
     double red[kTrB / 32];
 };
 
 // one CTA = kTrB samples; thread t owns sample blockIdx.x*kTrB + t
 template <bool kSig>
-__global__ void __launch_bounds__(kTrB) k_tr_step(VcbTrainParams P, long long step) {
+__global__ void __launch_bounds__(kTrB, 5) k_tr_step(VcbTrainParams P, long long step) {
     extern __shared__ __align__(16) unsigned char tr_smem[];
     TrSmem& S = *reinterpret_cast<TrSmem*>(tr_smem);
     const VcbField& F = P.model;
@@ -153,11 +152,11 @@ __global__ void __launch_bounds__(kTrB) k_tr_step(VcbTrainParams P, long long st
     }
     // rows for the CTA's weight-gradient reductions
 #pragma unroll
-    for (int m = 0; m < 16; m++) S.feat[t][m] = live ? feat[m] : 0.0f;
+    for (int m = 0; m < 16; m++) S.feat[m][t] = live ? feat[m] : 0.0f;
 #pragma unroll
     for (int j = 0; j < 32; j++) {
-        S.h0[t][j] = live ? h0[j] : 0.0f;
-        S.h1[t][j] = live ? h1[j] : 0.0f;
+        S.h0[j][t] = live ? h0[j] : 0.0f;
+        S.h1[j][t] = live ? h1[j] : 0.0f;
     }
     S.delta[t] = delta;
     // backward (mlp.py:64-74): d2 = (delta W2) * [h1 > 0]; d1 = (d2 W1) * [h0 > 0]; dfeat = d1 W0
@@ -165,7 +164,6 @@ __global__ void __launch_bounds__(kTrB) k_tr_step(VcbTrainParams P, long long st
 #pragma unroll
     for (int k = 0; k < 32; k++) {
         d2[k] = h1[k] > 0.0f ? delta * __ldg(W2 + k) : 0.0f;
-        S.d2[t][k] = live ? d2[k] : 0.0f;
     }
     float d1[32];
 #pragma unroll
@@ -174,7 +172,7 @@ __global__ void __launch_bounds__(kTrB) k_tr_step(VcbTrainParams P, long long st
 #pragma unroll
         for (int k = 0; k < 32; k++) a = __fmaf_rn(d2[k], __ldg(W1 + k * 32 + j), a);
         d1[j] = h0[j] > 0.0f ? a : 0.0f;
-        S.d1[t][j] = live ? d1[j] : 0.0f;
+        S.d1[j][t] = live ? d1[j] : 0.0f;
     }
     if (live) {
         float df[16];
@@ -235,23 +233,28 @@ __global__ void __launch_bounds__(kTrB) k_tr_step(VcbTrainParams P, long long st
         long long dst;
         if (e < 512) {  // dW0[j][m] = sum d1[j] feat[m]
             const int j = e >> 4, m = e & 15;
-            for (int s = 0; s < kTrB; s++) acc = __fmaf_rn(S.d1[s][j], S.feat[s][m], acc);
+            for (int s = 0; s < kTrB; s++) acc = __fmaf_rn(S.d1[j][s], S.feat[m][s], acc);
             dst = wbase + F.w_off[0] + e;
         } else if (e < 1536) {  // dW1[k][j] = sum d2[k] h0[j]
             const int q = e - 512, k = q >> 5, j = q & 31;
-            for (int s = 0; s < kTrB; s++) acc = __fmaf_rn(S.d2[s][k], S.h0[s][j], acc);
+            const float w2k = __ldg(W2 + k);
+            for (int s = 0; s < kTrB; s++) {
+                const float d2 = S.h1[k][s] > 0.0f ? S.delta[s] * w2k : 0.0f;  // (delta W2) * [h1 > 0]
+                acc = __fmaf_rn(d2, S.h0[j][s], acc);
+            }
             dst = wbase + F.w_off[1] + q;
         } else if (e < 1568) {  // dW2[k] = sum delta h1[k]
             const int k = e - 1536;
-            for (int s = 0; s < kTrB; s++) acc = __fmaf_rn(S.delta[s], S.h1[s][k], acc);
+            for (int s = 0; s < kTrB; s++) acc = __fmaf_rn(S.delta[s], S.h1[k][s], acc);
             dst = wbase + F.w_off[2] + k;
         } else if (e < 1600) {
             const int j = e - 1568;
-            for (int s = 0; s < kTrB; s++) acc = __fadd_rn(acc, S.d1[s][j]);
+            for (int s = 0; s < kTrB; s++) acc = __fadd_rn(acc, S.d1[j][s]);
             dst = bbase + F.b_off[0] + j;
         } else if (e < 1632) {
             const int k = e - 1600;
-            for (int s = 0; s < kTrB; s++) acc = __fadd_rn(acc, S.d2[s][k]);
+            const float w2k = __ldg(W2 + k);
+            for (int s = 0; s < kTrB; s++) acc = __fadd_rn(acc, S.h1[k][s] > 0.0f ? S.delta[s] * w2k : 0.0f);
             dst = bbase + F.b_off[1] + k;
         } else {
             for (int s = 0; s < kTrB; s++) acc = __fadd_rn(acc, S.delta[s]);
