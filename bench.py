@@ -423,6 +423,7 @@ def main():
         ucfg = SessionConfig(cached=False, loader="inline", cache=cfg.cache, scheduler=cfg.scheduler,
                              policy=cfg.policy, settings=cfg.settings, seed=0)
         usess = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), ucfg, macro=mg)
+        usess.impl = args.schedule
         ust = usess.stream
         uts, usamp = [], 0
         for i in range(args.uncached_steps + 1):

@@ -159,12 +159,13 @@ typedef struct {
     VcbFrameStats *stats;    /* device */
     void *workspace;
     int64_t workspace_bytes;
-    int32_t impl;            /* march schedule: 0 = one-barrier persistent wavefront, 384 threads/CTA
-                                (default), 1 = one launch per iteration, 2 = chained CTAs, 3 = persistent
-                                wavefront with look-back, 4 = two-phase persistent wavefront, 5/6/9 =
-                                schedule 0 with 768/640/512 threads/CTA, 7 = pipelined barrier-free,
-                                8 = schedule 0 with the majorants read through L1.  Path tracing:
-                                1 = two-barrier walk, otherwise the four-barrier walk */
+    int32_t impl;            /* march schedule.  Parity (the reference's RNG lanes = sample rank per
+                                wavefront iteration, sampler.py:206-213): 0 = one-barrier persistent
+                                wavefront, 384 threads/CTA (default), 9 = the same at 512 threads,
+                                1 = one launch per iteration (cross-check).  Throughput (RNG lane = film
+                                pixel, no grid barrier): 10/11/12 = one persistent ray per lane at
+                                512/768/1024 threads/CTA.  Path tracing: 1 = four-barrier walk,
+                                otherwise the default walk */
     int32_t image_global;    /* 0: image is this session's band [rows][W][4]; 1: image is the whole
                                 frame [height][W][4] (possibly a peer GPU's buffer mapped over NVLink)
                                 and local row j lands on film row row0 + j*row_step */

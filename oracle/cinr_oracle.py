@@ -430,6 +430,11 @@ class Config:
     adaptive: bool = True
     max_iterations: int = 8192
     macro_cell: int = 16
+    # stochastic-LoD RNG lanes: "rank" = the reference's (lane = rank of the sample among
+    # the samples of its wavefront iteration, sampler.py:206-213); "pixel" = the product's
+    # throughput schedule (lane = film pixel row*W+col, one xorshift32 step per sample of
+    # that ray; seeds and steps are sampler.py:39-58's)
+    rng: str = "rank"
 
 
 class OracleCache:
@@ -626,13 +631,16 @@ class OracleSession:
         else:
             self.scale = self.cfg.lod_scale
         self.rng = None
+        self.pixrng = None
         self.samples = 0
         self.true_misses = 0
         self.fallback_hits = 0
 
-    def _sample(self, pos, tmid):
+    def _sample(self, pos, tmid, pix=None):
         n = pos.shape[0]
-        if self.rng is None:
+        if self.cfg.rng == "pixel":
+            pass
+        elif self.rng is None:
             self.rng = lane_seeds(self.cfg.seed, self.frame, n)
         elif self.rng.shape[0] < n:
             raise AssertionError("lane pool outgrown (never happens in ray-march)")
@@ -649,7 +657,17 @@ class OracleSession:
             dist = np.linalg.norm(pos - np.asarray(self.camera[0], dtype=np.float64), axis=1)
         else:
             dist = np.ascontiguousarray(tmid)
-        u = xorshift_uniform(self.rng, n) if mode != 2 else np.zeros(n)
+        if mode == 2:
+            u = np.zeros(n)
+        elif self.cfg.rng == "pixel":
+            if self.pixrng is None:
+                W, H = self.camera[4], self.camera[5]
+                self.pixrng = lane_seeds(self.cfg.seed, self.frame, W * H)
+            st = self.pixrng[pix]
+            u = xorshift_uniform(st, n)
+            self.pixrng[pix] = st
+        else:
+            u = xorshift_uniform(self.rng, n)
         vals = np.empty(n, dtype=np.float32)
         served = np.empty(n, dtype=np.int8)
         req = np.empty(n, dtype=np.int8)
@@ -709,7 +727,7 @@ class OracleSession:
                 active &= ~dmask
                 rows = np.flatnonzero(smask)
                 if rows.size:
-                    vals = self._sample(np.ascontiguousarray(pbuf[rows]), tmb[rows])
+                    vals = self._sample(np.ascontiguousarray(pbuf[rows]), tmb[rows], pix=sel[rows])
                     dead = np.zeros(rows.size, dtype=np.bool_)
                     shade_pass(rows, np.ascontiguousarray(vals, dtype=np.float32), np.ascontiguousarray(dtb[rows]),
                                self.lut, cfg.adaptive, dt_base, cfg.term, color, trans, dead)

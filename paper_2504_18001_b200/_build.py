@@ -22,11 +22,8 @@ INCLUDE = PKG.parent / "include"
 SOURCES = {
     "capi.cu": [],
     "march.cu": ["-fmad=false"],
-    "chain.cu": ["-fmad=false"],
-    "wave.cu": ["-fmad=false"],
-    "wave2.cu": ["-fmad=false"],
     "wave3.cu": ["-fmad=false"],
-    "wave4.cu": ["-fmad=false"],
+    "rays.cu": ["-fmad=false"],
     "pt.cu": ["-fmad=false"],
     "train.cu": [],
     "decode.cu": [],

@@ -380,27 +380,19 @@ __global__ void k_frame_stats(VcbFrameParams p, FrameWs w, int kmax) {
 using namespace cinr;
 
 namespace cinr {
-int64_t chain_ws_bytes(int64_t npix, int max_it);
-int launch_chain_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev,
-                       int* ev_used);
-int launch_wave_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
-int launch_wave2_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
 int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
                        int nt, int mu_mode);
 int64_t wave3_ws_bytes(int64_t npix, int max_it);
-int64_t wave4_ws_bytes(int64_t npix, int max_it);
-int launch_wave4_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used);
+int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
+                     int nt);
 int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned int* out, int* live);
 int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* out);
 }  // namespace cinr
 
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
-    // the largest schedule layout (each includes frame_ws_layout)
-    int64_t a = wave3_ws_bytes(max_rays, max_iterations);
-    const int64_t a4 = wave4_ws_bytes(max_rays, max_iterations);
-    if (a4 > a) a = a4;
-    const int64_t b = chain_ws_bytes(max_rays, max_iterations);
-    return a > b ? a : b;
+    // the parity schedule's layout (includes frame_ws_layout; the throughput
+    // schedule uses only its counters)
+    return wave3_ws_bytes(max_rays, max_iterations);
 }
 
 extern "C" int32_t vcb_raygen_pass(int64_t n, const double* base, const double* rot, const double* origin,
@@ -489,14 +481,10 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
             }
         }
         cudaEvent_t* ev = p.timing ? g_ev.data() : nullptr;
-        if (p.impl == 2) return launch_chain_frame(p, st, &g_launches, ev, &g_ev_used);
-        if (p.impl == 3) return launch_wave_frame(p, st, &g_launches, ev, &g_ev_used);
-        if (p.impl == 4) return launch_wave2_frame(p, st, &g_launches, ev, &g_ev_used);
-        if (p.impl == 5) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 768, 0);
-        if (p.impl == 6) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 640, 0);
-        if (p.impl == 8) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 1);
         if (p.impl == 9) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
-        if (p.impl == 7) return launch_wave4_frame(p, st, &g_launches, ev, &g_ev_used);
+        if (p.impl == 10) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512);
+        if (p.impl == 11) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 768);
+        if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 1024);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;

@@ -1,0 +1,393 @@
+// Throughput-mode frame kernel ("fast path"), sm_100a, -fmad=false.
+//
+// One persistent CTA per SM; every lane owns one primary ray at a time and
+// marches it to completion with the ray state in registers:
+//
+//   ticket -> pixel (8x4 pixel tiles per warp, so a warp's rays stay coherent)
+//   raygen  (kernels.py:376-411; background for rays that miss the box)
+//   loop    advance (kernels.py:35-137) -> stochastic LoD + MRPD probe +
+//           trilinear + stamp + miss filing (kernels.py:166-273,
+//           sampler.py:236-275) -> true-miss inference (sampler.py:276-279)
+//           -> shade (kernels.py:322-355) -> early termination / iteration cap
+//           (raymarch.py:72-117)
+//   retire  rgb = color + T*bg, alpha = 1 - T (raymarch.py:57-60); the lane takes
+//           the next ticket.
+//
+// There is no grid barrier and no per-iteration state round trip through HBM:
+// the only global traffic is the sample's page-table entry and brick corners,
+// the miss counters and the retired pixel.  The per-sample arithmetic is the
+// parity path's (common.cuh) bit for bit; what differs is the RNG lane of the
+// stochastic LoD.  The reference numbers lanes by the sample's rank among the
+// samples of a wavefront iteration (sampler.py:206-213, P5), which needs a
+// grid-wide scan per iteration.  Here lane = the ray's global film pixel
+// (row * W + column): seed lane_seed(frame base, pixel) (sampler.py:39-45),
+// one xorshift32 step per sample of that ray (sampler.py:51-58).  Same
+// per-sample distribution (E[LoD] = D), and it needs no ordering, so band
+// partitions of a frame draw exactly the numbers the whole frame would.  With
+// LodPolicy(mode="off") no number is drawn and frames are bit-identical to the
+// parity schedule (images, counters, stamps, miss reports).
+//
+// True misses are inferred by the warp that meets them: for the default INR the
+// whole warp runs the tensor-core inference (mlp_warp.cuh, 32 samples per call)
+// whenever any lane holds a miss, so its values are the parity path's.
+#include <cstdio>
+
+#include "common.cuh"
+#include "fields.cuh"
+#include "march.cuh"
+#include "mlp_warp.cuh"
+
+namespace cinr {
+
+struct RmCfg {
+    int sm_lut, sm_mu, sm_occ, sm_mlp;  // dynamic shared-memory offsets (-1 = not staged)
+    int tiles_x;                         // 8-pixel tile columns
+    int max_it;
+    long long n_tickets;                 // 32 per 8x4 tile
+};
+
+struct RmSmem {
+    unsigned long long cnt[5];  // exact, fallback, miss, samples, rays
+    int max_k;
+};
+
+__device__ __forceinline__ void rm_retire(const VcbFrameParams& p, long long pix, double cr, double cg, double cb,
+                                          double tr) {
+    // raymarch.py:57-60: rgb = color + T*bg, alpha = 1 - T, then .astype(float32)
+    float4 o;
+    o.x = __double2float_rn(DADD(cr, DMUL(tr, p.bg[0])));
+    o.y = __double2float_rn(DADD(cg, DMUL(tr, p.bg[1])));
+    o.z = __double2float_rn(DADD(cb, DMUL(tr, p.bg[2])));
+    o.w = __double2float_rn(DSUB(1.0, tr));
+    reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = o;
+}
+
+// The default INR at 32 positions of the warp (out of line: the inference's
+// registers do not count against the march loop's budget).  Called converged.
+static __device__ __noinline__ float rm_infer_warp(const VcbField& F, const MlpFrag* fr, double x, double y,
+                                                   double z) {
+    return inr_warp_default(F, fr, x, y, z);
+}
+
+template <int kInr>
+static __device__ __noinline__ float rm_infer_lane(const VcbField& F, double x, double y, double z,
+                                                   const MlpSmem m, int* bad) {
+    return field_eval<kInr>(F, x, y, z, m, bad);
+}
+
+template <int kInr, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_ray_march(const __grid_constant__ VcbFrameParams p, FrameCounters* ctr, const __grid_constant__ RmCfg cfg) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ RmSmem sm;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const double hmax = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
+
+    // ---- read-only tables in shared memory: LUT, majorants (or occupancy bits), MLP
+    float* s_lut = cfg.sm_lut >= 0 ? reinterpret_cast<float*>(dsm + cfg.sm_lut) : nullptr;
+    if (s_lut)
+        for (int i = threadIdx.x; i < p.lut_size * 4; i += NT) s_lut[i] = __ldg(p.lut + i);
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    const float* mu_s = nullptr;
+    const uint32_t* occ = nullptr;
+    if (cfg.sm_mu >= 0) {
+        float* m = reinterpret_cast<float*>(dsm + cfg.sm_mu);
+        for (long long i = threadIdx.x; i < cells; i += NT) m[i] = __ldg(p.mu + i);
+        mu_s = m;
+    } else if (cfg.sm_occ >= 0) {
+        uint32_t* o = reinterpret_cast<uint32_t*>(dsm + cfg.sm_occ);
+        const int nwords = (int)((cells + 31) >> 5);
+        for (int wd = threadIdx.x >> 5; wd < nwords; wd += NT / 32) {
+            const long long q = (long long)wd * 32 + lane;
+            const unsigned b = __ballot_sync(0xffffffffu, q < cells && __ldg(p.mu + q) > 0.0f);
+            if (lane == 0) o[wd] = b;
+        }
+        occ = o;
+    }
+    MlpSmem mlp;
+    mlp.w = mlp.b = nullptr;
+    const MlpFrag* mfrag = nullptr;
+    if (kInr == 1 && cfg.sm_mlp >= 0) {
+        stage_mlp_frag(p.field, reinterpret_cast<MlpFrag*>(dsm + cfg.sm_mlp));
+        mfrag = reinterpret_cast<const MlpFrag*>(dsm + cfg.sm_mlp);
+    } else if (kInr != 0 && cfg.sm_mlp >= 0) {
+        stage_mlp(p.field, reinterpret_cast<float*>(dsm + cfg.sm_mlp), mlp);
+    }
+    if (threadIdx.x < 5) sm.cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sm.max_k = 0;
+    __syncthreads();
+    const float* lut = s_lut ? s_lut : p.lut;
+
+    const double ox = p.cam.origin[0], oy = p.cam.origin[1], oz = p.cam.origin[2];
+    const int W = p.cam.width, H = p.cam.height, rows = p.cam.rows;
+    const bool use_rng = p.cached && p.probe.mode != 2;
+    const bool adaptive = p.adv.adaptive != 0;
+
+    // per-lane ray state
+    bool has = false;
+    int k = 0;               // samples taken by the lane's ray (the wavefront iteration index)
+    long long pix = 0;       // local (band) pixel index
+    double dx = 0.0, dy = 0.0, dz = 0.0, ten = 0.0, tex = 0.0;
+    long long cur = 0;       // cursor_f bits (adaptive) or cursor_k
+    double cr = 0.0, cg = 0.0, cb = 0.0, tr = 1.0;
+    uint32_t rs = 0u;
+    unsigned c_ex = 0, c_fb = 0, c_ms = 0, c_rays = 0;
+    unsigned long long c_smp = 0;
+    int max_k = 0, bad = 0;
+    bool exhausted = false;
+    const float4 bgv = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+
+    for (;;) {
+        // ---- refill: lanes without a ray take the next tickets (one atomic per warp)
+        while (!exhausted) {
+            const unsigned need = __ballot_sync(0xffffffffu, !has);
+            if (!need) break;
+            long long base = 0;
+            if (lane == 0) base = atomicAdd(&ctr->ticket_rays, __popc(need));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= cfg.n_tickets) {
+                exhausted = true;
+                break;
+            }
+            if (!has) {
+                const long long t = base + __popc(need & lt_mask);
+                if (t < cfg.n_tickets) {
+                    const long long tile = t >> 5;
+                    const int within = (int)(t & 31);
+                    const int x = (int)(tile % cfg.tiles_x) * 8 + (within & 7);
+                    const int yl = (int)(tile / cfg.tiles_x) * 4 + (within >> 3);
+                    if (x < W && yl < rows) {
+                        const int film_row = p.cam.row0 + yl * p.cam.row_step;
+                        double fx, fy;
+                        film_coord(x, film_row, W, H, fx, fy);
+                        const Ray r = make_ray(fx, fy, p.cam);
+                        pix = (long long)yl * W + x;
+                        if (r.keep) {
+                            has = true;
+                            k = 0;
+                            dx = r.dx;
+                            dy = r.dy;
+                            dz = r.dz;
+                            ten = r.t0;
+                            tex = r.t1;
+                            cur = adaptive ? __double_as_longlong(r.t0) : 0ll;
+                            cr = cg = cb = 0.0;
+                            tr = 1.0;
+                            c_rays++;
+                            if (use_rng) rs = lane_seed(p.rng_base, (u64)((long long)film_row * W + x));
+                        } else {
+                            // raymarch.py:33-35 background, alpha 0
+                            reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = bgv;
+                        }
+                    }
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, has)) break;
+
+        // ---- advance (or the iteration-cap flush, raymarch.py:117)
+        int samp = 0;
+        AdvanceOut a;
+        a.px = a.py = a.pz = 0.5;
+        a.dt = a.tmid = 0.0;
+        if (has) {
+            int f = 0;
+            if (k < cfg.max_it) {
+                double cf = __longlong_as_double(cur);
+                i64 ck = cur;
+                f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s);
+                cur = adaptive ? __double_as_longlong(cf) : (long long)ck;
+            }
+            if (f) {
+                samp = 1;
+                k++;
+            } else {
+                rm_retire(p, pix, cr, cg, cb, tr);
+                has = false;
+                max_k = max(max_k, k);
+            }
+        }
+
+        // ---- probe (stochastic LoD, MRPD walk, trilinear, stamp, miss filing)
+        float v = 0.0f;
+        int needinf = 0;
+        if (samp) {
+            c_smp++;
+            if (!p.cached) {
+                needinf = 1;
+            } else {
+                double u = 0.0;
+                if (use_rng) {
+                    rs = xorshift32(rs);
+                    u = DMUL((double)rs, 2.3283064365386963e-10);  // / 2^32, exact
+                }
+                double dist = a.tmid;
+                if (p.paged_dist) {
+                    const double ex = DSUB(a.px, ox), ey = DSUB(a.py, oy), ez = DSUB(a.pz, oz);
+                    dist = __dsqrt_rn(DADD(DADD(DMUL(ex, ex), DMUL(ey, ey)), DMUL(ez, ez)));
+                }
+                int rq, slot;
+                const int sv = probe_one(a.px, a.py, a.pz, dist, u, p.probe, p.table, p.pool,
+                                         (long long*)p.last_used, p.cache_frame, v, rq, slot);
+                if (sv != rq) {
+                    // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
+                    const i64 span = p.probe.b << rq;
+                    const double nx = clampd(DSUB(DMUL(a.px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
+                    const double ny = clampd(DSUB(DMUL(a.py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
+                    const double nz = clampd(DSUB(DMUL(a.pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
+                    const i64 bx =
+                        clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, p.probe.grid[rq][0] - 1);
+                    const i64 by =
+                        clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, p.probe.grid[rq][1] - 1);
+                    const i64 bz =
+                        clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, p.probe.grid[rq][2] - 1);
+                    warp_aggregated_add(p.miss_count,
+                                        p.probe.offset[rq] + bx + p.probe.grid[rq][0] * (by + p.probe.grid[rq][1] * bz));
+                }
+                if (sv < 0) {
+                    needinf = 1;
+                } else {
+                    c_ex += (sv == rq);
+                    c_fb += (sv != rq);
+                }
+            }
+        }
+
+        // ---- true-miss inference (sampler.py:276-279): clip(world, 0, nextafter(1, 0))
+        if (kInr == 1) {
+            if (__any_sync(0xffffffffu, needinf)) {
+                const double qx = needinf ? clampd(a.px, 0.0, hmax) : 0.5;
+                const double qy = needinf ? clampd(a.py, 0.0, hmax) : 0.5;
+                const double qz = needinf ? clampd(a.pz, 0.0, hmax) : 0.5;
+                float vi = rm_infer_warp(p.field, mfrag, qx, qy, qz);
+                if (needinf) {
+                    if (!isfinite(vi)) bad = 1;
+                    if (p.field.clip01) vi = vi < 0.0f ? 0.0f : (vi > 1.0f ? 1.0f : vi);
+                    v = vi;
+                }
+            }
+        } else if (needinf) {
+            v = rm_infer_lane<kInr>(p.field, clampd(a.px, 0.0, hmax), clampd(a.py, 0.0, hmax),
+                                    clampd(a.pz, 0.0, hmax), mlp, &bad);
+        }
+        c_ms += needinf;
+
+        // ---- shade + early termination
+        if (samp) {
+            const bool dead = s_lut ? shade_one<true>(v, a.dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base,
+                                                      p.term, cr, cg, cb, tr)
+                                    : shade_one<false>(v, a.dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base,
+                                                       p.term, cr, cg, cb, tr);
+            if (dead) {
+                rm_retire(p, pix, cr, cg, cb, tr);
+                has = false;
+                max_k = max(max_k, k);
+            }
+        }
+    }
+
+    // ---- frame counters (FrameStats, mrpd.py:33-41)
+    if (bad) atomicExch((unsigned long long*)&p.stats->nonfinite, 1ull);
+    const unsigned long long t_ex = warp_sum((unsigned long long)c_ex);
+    const unsigned long long t_fb = warp_sum((unsigned long long)c_fb);
+    const unsigned long long t_ms = warp_sum((unsigned long long)c_ms);
+    const unsigned long long t_sm = warp_sum(c_smp);
+    const unsigned long long t_ry = warp_sum((unsigned long long)c_rays);
+    int mk = max_k;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+    if (lane == 0) {
+        atomicAdd(&sm.cnt[0], t_ex);
+        atomicAdd(&sm.cnt[1], t_fb);
+        atomicAdd(&sm.cnt[2], t_ms);
+        atomicAdd(&sm.cnt[3], t_sm);
+        atomicAdd(&sm.cnt[4], t_ry);
+        atomicMax(&sm.max_k, mk);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        VcbFrameStats* S = p.stats;
+        atomicAdd((unsigned long long*)&S->exact, sm.cnt[0]);
+        atomicAdd((unsigned long long*)&S->fallback, sm.cnt[1]);
+        atomicAdd((unsigned long long*)&S->miss, sm.cnt[2]);
+        atomicAdd((unsigned long long*)&S->misses_resolved, sm.cnt[2]);
+        atomicAdd((unsigned long long*)&S->requests, sm.cnt[3]);
+        atomicAdd((unsigned long long*)&S->rays, sm.cnt[4]);
+        // wavefront iterations the parity schedule runs: the longest ray's samples + 1
+        if (sm.cnt[4]) atomicMax((long long*)&S->iterations, (long long)sm.max_k + 1);
+    }
+}
+
+static const void* ray_kernel(int mode, int nt) {
+    if (nt == 1024)
+        return mode == 1 ? (const void*)k_ray_march<1, 1024>
+                         : mode == 2 ? (const void*)k_ray_march<2, 1024> : (const void*)k_ray_march<0, 1024>;
+    if (nt == 768)
+        return mode == 1 ? (const void*)k_ray_march<1, 768>
+                         : mode == 2 ? (const void*)k_ray_march<2, 768> : (const void*)k_ray_march<0, 768>;
+    return mode == 1 ? (const void*)k_ray_march<1, 512>
+                     : mode == 2 ? (const void*)k_ray_march<2, 512> : (const void*)k_ray_march<0, 512>;
+}
+
+// nt: threads per CTA (one CTA per SM)
+int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
+                     int nt) {
+    const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
+    const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
+    FrameWs w;
+    const int64_t need = frame_ws_layout(0, max_it, p.workspace, &w);
+    if (need > p.workspace_bytes)
+        return set_error("march_frame: workspace too small (%lld < %lld)", (long long)p.workspace_bytes,
+                         (long long)need);
+    const int mode = inr_mode(p.field);
+    RmCfg cfg;
+    cfg.max_it = max_it;
+    cfg.tiles_x = (p.cam.width + 7) / 8;
+    cfg.n_tickets = (long long)cfg.tiles_x * ((p.cam.rows + 3) / 4) * 32;
+    if (cfg.n_tickets >= (1ll << 31)) return set_error("march_frame: %lld pixels exceed the ticket range", (long long)npix);
+    int off = 0;
+    auto take = [&](int bytes) {
+        const int o = (off + 15) & ~15;
+        off = o + bytes;
+        return o;
+    };
+    constexpr int kSmemMax = 227 * 1024;
+    cfg.sm_lut = (p.lut_size <= 4096) ? take(p.lut_size * 16) : -1;
+    cfg.sm_mlp = -1;
+    if (p.field.kind == 0) {
+        int nw = 0, nb = 0;
+        for (int L = 0; L < p.field.n_layers; L++) {
+            nw += p.field.widths[L] * p.field.widths[L + 1];
+            nb += p.field.widths[L + 1];
+        }
+        cfg.sm_mlp = take(mode == 1 ? (int)sizeof(MlpFrag) : (nw + nb) * 4);
+    }
+    const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
+    cfg.sm_mu = cfg.sm_occ = -1;
+    if (off + 16 + cells * 4 <= kSmemMax) cfg.sm_mu = take((int)cells * 4);
+    else if (p.adv.skip_empty && off + 16 + ((cells + 31) >> 5) * 4 <= kSmemMax)
+        cfg.sm_occ = take((int)(((cells + 31) >> 5) * 4));
+    if (mode == 2) nt = 512;
+    const void* fn = ray_kernel(mode, nt);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, off);
+    if (per_sm < 1) return set_error("march_frame: ray kernel does not fit one CTA per SM (%d B shared)", off);
+    cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
+    const int G = device_sms();
+    VcbFrameParams pc = p;
+    FrameCounters* ctr = w.ctr;
+    void* args[3] = {&pc, &ctr, &cfg};
+    if (ev) cudaEventRecord(ev[0], st);
+    cudaError_t e = cudaLaunchKernel(fn, G, nt, args, off, st);
+    if (ev) {
+        cudaEventRecord(ev[1], st);
+        *ev_used = 1;
+    }
+    if (e != cudaSuccess) return set_error("march_frame: ray kernel launch: %s", cudaGetErrorString(e));
+    *launches = 1;
+    return check_launch("march_frame(rays)");
+}
+
+}  // namespace cinr

@@ -745,8 +745,6 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 static const void* wave3_kernel(int mode, int nt) {
-    if (nt == 768) return mode == 1 ? (const void*)k_wave3_march<1, 768> : (const void*)k_wave3_march<0, 768>;
-    if (nt == 640) return mode == 1 ? (const void*)k_wave3_march<1, 640> : (const void*)k_wave3_march<0, 640>;
     if (nt == 384) return mode == 1 ? (const void*)k_wave3_march<1, 384> : (const void*)k_wave3_march<0, 384>;
     return mode == 1 ? (const void*)k_wave3_march<1, 512>
                      : mode == 2 ? (const void*)k_wave3_march<2, 512> : (const void*)k_wave3_march<0, 512>;

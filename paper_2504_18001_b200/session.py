@@ -74,7 +74,7 @@ class RenderSession:
     """Owns the device render state for one viewer/bench run."""
 
     def __init__(self, field_src, tf, camera, config: SessionConfig, macro=None, device=None, debug=False,
-                 stream=None):
+                 stream=None, march="parity"):
         self.device = require_cuda(device)
         if config.mode not in ("raymarch", "pathtrace"):
             raise ValueError(f"unknown mode {config.mode!r}")
@@ -107,10 +107,31 @@ class RenderSession:
         self.last_frame_stats = {}
         self.timing = False  # CUDA-event time the frame kernel (bench)
         self.trace = False  # record the per-iteration trace (diagnostics)
-        self.impl = 0  # march schedule (VcbFrameParams.impl): 0 = one-barrier persistent wavefront
+        self.impl = 0  # march schedule (VcbFrameParams.impl), set through `march`
+        self.march = march
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
         self._target = None  # whole-frame buffer written in place (fused sort-first gather)
         self._pin_free = []  # pinned host frames released by callers
+
+    MARCH_SCHEDULES = {"parity": 0, "throughput": 10}
+
+    @property
+    def march(self) -> str:
+        """Frame-kernel schedule: "parity" (default) numbers the stochastic-LoD RNG lanes
+        by sample rank per wavefront iteration exactly as the reference (sampler.py:206-213),
+        so cache state is bit-exact; "throughput" marches one persistent ray per GPU lane
+        with lane = film pixel (same per-sample distribution, no grid barriers; bit-exact
+        with "parity" when LodPolicy.mode == "off")."""
+        for k, v in self.MARCH_SCHEDULES.items():
+            if v == self.impl:
+                return k
+        return f"impl{self.impl}"
+
+    @march.setter
+    def march(self, name: str):
+        if name not in self.MARCH_SCHEDULES:
+            raise ValueError(f"unknown march schedule {name!r} (parity | throughput)")
+        self.impl = self.MARCH_SCHEDULES[name]
 
     def set_band(self, row0: int, row_step: int):
         """Render only film rows row0 + j*row_step (one rank's share of a frame)."""

@@ -38,7 +38,7 @@ def oracle_config(spec):
         lod_scale=pol.get("lod_scale", 1.0), preload=pol.get("preload_frames", 120), mode=pol.get("mode", "corrected"),
         cached=spec.get("cached", True), seed=spec.get("seed", 0),
         skip_empty=st.get("skip_empty", True), adaptive=st.get("adaptive_step", True),
-        base_step_scale=st.get("base_step_scale", 0.5),
+        base_step_scale=st.get("base_step_scale", 0.5), rng=spec.get("rng", "rank"),
     )
 
 

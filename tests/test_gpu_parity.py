@@ -212,10 +212,10 @@ def test_session_vs_oracle_random_scene(seed):
         scene_specs.SESSION_SPECS.pop(name, None)
 
 
-@pytest.mark.parametrize("other", [1, 2, 3, 4, 7, 9])
+@pytest.mark.parametrize("other", [1, 9])
 def test_march_schedules_agree(other):
     """The persistent wavefront (default), the launch-per-iteration wavefront and
-    the chained-CTA march are schedules of the same arithmetic: identical images
+    the 512-thread build are schedules of the same arithmetic: identical images
     and cache state."""
     from gpu_runner import run_gpu_session
 
