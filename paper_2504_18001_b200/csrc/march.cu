@@ -384,7 +384,8 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
                        int nt, int mu_mode);
 int64_t wave3_ws_bytes(int64_t npix, int max_it);
 int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
-                     int nt);
+                     int nt, int max_skip);
+int64_t rays_ws_bytes(int64_t npix, int max_it);
 int wave3_trace(const void* workspace, int64_t npix, int max_it, int n, unsigned int* out, int* live);
 int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* out);
 }  // namespace cinr
@@ -392,7 +393,8 @@ int wave3_counters(const void* workspace, int64_t npix, int max_it, long long* o
 extern "C" int64_t vcb_frame_workspace_bytes(int64_t max_rays, int32_t max_iterations) {
     // the parity schedule's layout (includes frame_ws_layout; the throughput
     // schedule uses only its counters)
-    return wave3_ws_bytes(max_rays, max_iterations);
+    const int64_t a = wave3_ws_bytes(max_rays, max_iterations), b = rays_ws_bytes(max_rays, max_iterations);
+    return a > b ? a : b;
 }
 
 extern "C" int32_t vcb_raygen_pass(int64_t n, const double* base, const double* rot, const double* origin,
@@ -482,9 +484,11 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         }
         cudaEvent_t* ev = p.timing ? g_ev.data() : nullptr;
         if (p.impl == 9) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
-        if (p.impl == 10) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512);
-        if (p.impl == 11) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 768);
-        if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 1024);
+        if (p.impl == 10) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 2);
+        if (p.impl == 11) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 1);
+        if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 4);
+        if (p.impl == 13) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
+        if (p.impl == 14) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 1024, 2);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;

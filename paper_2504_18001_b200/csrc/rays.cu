@@ -43,8 +43,64 @@ struct RmCfg {
     int sm_lut, sm_mu, sm_occ, sm_mlp;  // dynamic shared-memory offsets (-1 = not staged)
     int tiles_x;                         // 8-pixel tile columns
     int max_it;
+    int max_skip;                        // empty macro cells one lane crosses per loop turn (0 = all)
     long long n_tickets;                 // 32 per 8x4 tile
+    double4* ray_a;                      // [n] dx, dy, dz, t_enter of the box-hitting rays
+    double2* ray_b;                      // [n] t_exit, (local pixel, film pixel) as two int32
+    int* n_rays;                         // rays in the list (written by k_ray_setup)
 };
+
+// workspace after frame_ws_layout(0, ...): the ray list
+inline int64_t rays_layout(int64_t npix, void* base, RmCfg* c) {
+    const size_t a = align_up((size_t)npix * sizeof(double4), 256);
+    const size_t b = align_up((size_t)npix * sizeof(double2), 256);
+    if (base && c) {
+        c->ray_a = reinterpret_cast<double4*>(base);
+        c->ray_b = reinterpret_cast<double2*>((char*)base + a);
+    }
+    return (int64_t)(a + b);
+}
+
+int64_t rays_ws_bytes(int64_t npix, int max_it) {
+    if (max_it > kMaxIterCap) max_it = kMaxIterCap;
+    return frame_ws_layout(0, max_it, nullptr, nullptr) + rays_layout(npix, nullptr, nullptr);
+}
+
+// Ray setup (kernels.py:376-411, camera.py:129-154): tickets walk 8x4 pixel tiles; box
+// hits are appended to the ray list warp by warp (list order is irrelevant here: the
+// RNG lane is the pixel), every other pixel gets the background (raymarch.py:33-35).
+__global__ void __launch_bounds__(256) k_ray_setup(const __grid_constant__ VcbFrameParams p, RmCfg cfg) {
+    const int lane = threadIdx.x & 31;
+    const int W = p.cam.width, H = p.cam.height, rows = p.cam.rows;
+    const float4 bgv = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < cfg.n_tickets; t0 += stride) {
+        const long long t = t0 + lane;
+        const long long tile = t >> 5;
+        const int x = (int)(tile % cfg.tiles_x) * 8 + (lane & 7);
+        const int yl = (int)(tile / cfg.tiles_x) * 4 + (lane >> 3);
+        bool keep = false;
+        Ray r;
+        int film_row = 0;
+        if (x < W && yl < rows) {
+            film_row = p.cam.row0 + yl * p.cam.row_step;
+            double fx, fy;
+            film_coord(x, film_row, W, H, fx, fy);
+            r = make_ray(fx, fy, p.cam);
+            keep = r.keep;
+            if (!keep) reinterpret_cast<float4*>(p.image)[frame_pixel(p, (long long)yl * W + x)] = bgv;
+        }
+        const unsigned kb = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && kb) base = atomicAdd(cfg.n_rays, __popc(kb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+            const int j = base + __popc(kb & ((1u << lane) - 1u));
+            cfg.ray_a[j] = make_double4(r.dx, r.dy, r.dz, r.t0);
+            cfg.ray_b[j] = make_double2(r.t1, __hiloint2double(film_row * W + x, yl * W + x));
+        }
+    }
+}
 
 struct RmSmem {
     unsigned long long cnt[5];  // exact, fallback, miss, samples, rays
@@ -120,7 +176,6 @@ __global__ void __launch_bounds__(NT, 1)
     const float* lut = s_lut ? s_lut : p.lut;
 
     const double ox = p.cam.origin[0], oy = p.cam.origin[1], oz = p.cam.origin[2];
-    const int W = p.cam.width, H = p.cam.height, rows = p.cam.rows;
     const bool use_rng = p.cached && p.probe.mode != 2;
     const bool adaptive = p.adv.adaptive != 0;
 
@@ -135,58 +190,45 @@ __global__ void __launch_bounds__(NT, 1)
     unsigned c_ex = 0, c_fb = 0, c_ms = 0, c_rays = 0;
     unsigned long long c_smp = 0;
     int max_k = 0, bad = 0;
-    bool exhausted = false;
-    const float4 bgv = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+    const long long n_list = __ldcg(cfg.n_rays);
+    bool exhausted = n_list == 0;
 
     for (;;) {
-        // ---- refill: lanes without a ray take the next tickets (one atomic per warp)
-        while (!exhausted) {
+        // ---- refill: lanes without a ray take the next rays of the list (one atomic per warp)
+        if (!exhausted) {
             const unsigned need = __ballot_sync(0xffffffffu, !has);
-            if (!need) break;
-            long long base = 0;
-            if (lane == 0) base = atomicAdd(&ctr->ticket_rays, __popc(need));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (base >= cfg.n_tickets) {
-                exhausted = true;
-                break;
-            }
-            if (!has) {
-                const long long t = base + __popc(need & lt_mask);
-                if (t < cfg.n_tickets) {
-                    const long long tile = t >> 5;
-                    const int within = (int)(t & 31);
-                    const int x = (int)(tile % cfg.tiles_x) * 8 + (within & 7);
-                    const int yl = (int)(tile / cfg.tiles_x) * 4 + (within >> 3);
-                    if (x < W && yl < rows) {
-                        const int film_row = p.cam.row0 + yl * p.cam.row_step;
-                        double fx, fy;
-                        film_coord(x, film_row, W, H, fx, fy);
-                        const Ray r = make_ray(fx, fy, p.cam);
-                        pix = (long long)yl * W + x;
-                        if (r.keep) {
-                            has = true;
-                            k = 0;
-                            dx = r.dx;
-                            dy = r.dy;
-                            dz = r.dz;
-                            ten = r.t0;
-                            tex = r.t1;
-                            cur = adaptive ? __double_as_longlong(r.t0) : 0ll;
-                            cr = cg = cb = 0.0;
-                            tr = 1.0;
-                            c_rays++;
-                            if (use_rng) rs = lane_seed(p.rng_base, (u64)((long long)film_row * W + x));
-                        } else {
-                            // raymarch.py:33-35 background, alpha 0
-                            reinterpret_cast<float4*>(p.image)[frame_pixel(p, pix)] = bgv;
-                        }
+            if (need) {
+                long long base = 0;
+                if (lane == 0) base = atomicAdd(&ctr->ticket_rays, __popc(need));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base + __popc(need) >= n_list) exhausted = true;
+                if (!has) {
+                    const long long t = base + __popc(need & lt_mask);
+                    if (t < n_list) {
+                        const double2* pa = reinterpret_cast<const double2*>(cfg.ray_a + t);
+                        const double2 ra0 = __ldcs(pa), ra1 = __ldcs(pa + 1);
+                        const double2 rb = __ldcs(cfg.ray_b + t);
+                        has = true;
+                        k = 0;
+                        dx = ra0.x;
+                        dy = ra0.y;
+                        dz = ra1.x;
+                        ten = ra1.y;
+                        tex = rb.x;
+                        pix = __double2loint(rb.y);
+                        cur = adaptive ? __double_as_longlong(ten) : 0ll;
+                        cr = cg = cb = 0.0;
+                        tr = 1.0;
+                        c_rays++;
+                        if (use_rng) rs = lane_seed(p.rng_base, (u64)(unsigned)__double2hiint(rb.y));
                     }
                 }
             }
         }
         if (!__any_sync(0xffffffffu, has)) break;
 
-        // ---- advance (or the iteration-cap flush, raymarch.py:117)
+        // ---- advance (or the iteration-cap flush, raymarch.py:117); a lane crossing empty
+        // space stops after max_skip cells and resumes the same advance next turn
         int samp = 0;
         AdvanceOut a;
         a.px = a.py = a.pz = 0.5;
@@ -196,10 +238,13 @@ __global__ void __launch_bounds__(NT, 1)
             if (k < cfg.max_it) {
                 double cf = __longlong_as_double(cur);
                 i64 ck = cur;
-                f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s);
+                f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
+                                cfg.max_skip);
                 cur = adaptive ? __double_as_longlong(cf) : (long long)ck;
             }
-            if (f) {
+            if (f == 2) {
+                // mid-advance: no sample this turn
+            } else if (f) {
                 samp = 1;
                 k++;
             } else {
@@ -323,28 +368,28 @@ static const void* ray_kernel(int mode, int nt) {
     if (nt == 1024)
         return mode == 1 ? (const void*)k_ray_march<1, 1024>
                          : mode == 2 ? (const void*)k_ray_march<2, 1024> : (const void*)k_ray_march<0, 1024>;
-    if (nt == 768)
-        return mode == 1 ? (const void*)k_ray_march<1, 768>
-                         : mode == 2 ? (const void*)k_ray_march<2, 768> : (const void*)k_ray_march<0, 768>;
     return mode == 1 ? (const void*)k_ray_march<1, 512>
                      : mode == 2 ? (const void*)k_ray_march<2, 512> : (const void*)k_ray_march<0, 512>;
 }
 
-// nt: threads per CTA (one CTA per SM)
+// nt: threads per CTA (one CTA per SM); max_skip: see advance_impl
 int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
-                     int nt) {
+                     int nt, int max_skip) {
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
     const int max_it = p.max_iterations < kMaxIterCap ? p.max_iterations : kMaxIterCap;
     FrameWs w;
-    const int64_t need = frame_ws_layout(0, max_it, p.workspace, &w);
+    const int64_t need0 = frame_ws_layout(0, max_it, p.workspace, &w);
+    RmCfg cfg;
+    const int64_t need = need0 + rays_layout(npix, (char*)p.workspace + need0, &cfg);
     if (need > p.workspace_bytes)
         return set_error("march_frame: workspace too small (%lld < %lld)", (long long)p.workspace_bytes,
                          (long long)need);
     const int mode = inr_mode(p.field);
-    RmCfg cfg;
     cfg.max_it = max_it;
+    cfg.max_skip = max_skip;
     cfg.tiles_x = (p.cam.width + 7) / 8;
     cfg.n_tickets = (long long)cfg.tiles_x * ((p.cam.rows + 3) / 4) * 32;
+    cfg.n_rays = &w.ctr->pad[0];
     if (cfg.n_tickets >= (1ll << 31)) return set_error("march_frame: %lld pixels exceed the ticket range", (long long)npix);
     int off = 0;
     auto take = [&](int bytes) {
@@ -376,17 +421,18 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     if (per_sm < 1) return set_error("march_frame: ray kernel does not fit one CTA per SM (%d B shared)", off);
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     const int G = device_sms();
+    if (ev) cudaEventRecord(ev[0], st);
+    k_ray_setup<<<grid_for(cfg.n_tickets, 256), 256, 0, st>>>(p, cfg);
     VcbFrameParams pc = p;
     FrameCounters* ctr = w.ctr;
     void* args[3] = {&pc, &ctr, &cfg};
-    if (ev) cudaEventRecord(ev[0], st);
     cudaError_t e = cudaLaunchKernel(fn, G, nt, args, off, st);
     if (ev) {
         cudaEventRecord(ev[1], st);
         *ev_used = 1;
     }
     if (e != cudaSuccess) return set_error("march_frame: ray kernel launch: %s", cudaGetErrorString(e));
-    *launches = 1;
+    *launches = 2;
     return check_launch("march_frame(rays)");
 }
 
