@@ -486,9 +486,9 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 9) return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
         if (p.impl == 10) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 2);
         if (p.impl == 11) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 1);
-        if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 4);
+        if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 640, 1);
         if (p.impl == 13) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
-        if (p.impl == 14) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 1024, 2);
+        if (p.impl == 14) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 640, 2);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;

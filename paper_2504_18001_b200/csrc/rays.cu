@@ -131,7 +131,11 @@ static __device__ __noinline__ float rm_infer_lane(const VcbField& F, double x, 
     return field_eval<kInr>(F, x, y, z, m, bad);
 }
 
-template <int kInr, int NT>
+// kFast = 1: majorants and LUT in shared memory, adaptive steps, empty-space
+// skipping (every BASELINE config): the run-time switches are folded away, which
+// halves the loop's code (instruction-cache misses were a fifth of the stalls).
+// (Memoising the adaptive step's division per ray costs 5 registers and spills: slower.)
+template <int kInr, int NT, int kFast>
 __global__ void __launch_bounds__(NT, 1)
     k_ray_march(const __grid_constant__ VcbFrameParams p, FrameCounters* ctr, const __grid_constant__ RmCfg cfg) {
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -238,8 +242,12 @@ __global__ void __launch_bounds__(NT, 1)
             if (k < cfg.max_it) {
                 double cf = __longlong_as_double(cur);
                 i64 ck = cur;
-                f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
-                                cfg.max_skip);
+                if constexpr (kFast)
+                    f = advance_impl<1>(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
+                                        cfg.max_skip);
+                else
+                    f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
+                                    cfg.max_skip);
                 cur = adaptive ? __double_as_longlong(cf) : (long long)ck;
             }
             if (f == 2) {
@@ -320,8 +328,8 @@ __global__ void __launch_bounds__(NT, 1)
 
         // ---- shade + early termination
         if (samp) {
-            const bool dead = s_lut ? shade_one<true>(v, a.dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base,
-                                                      p.term, cr, cg, cb, tr)
+            const bool dead = (kFast || s_lut) ? shade_one<true>(v, a.dt, lut, p.lut_size, kFast ? 1 : p.adv.adaptive,
+                                                                 p.adv.dt_base, p.term, cr, cg, cb, tr)
                                     : shade_one<false>(v, a.dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base,
                                                        p.term, cr, cg, cb, tr);
             if (dead) {
@@ -364,12 +372,16 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-static const void* ray_kernel(int mode, int nt) {
-    if (nt == 1024)
-        return mode == 1 ? (const void*)k_ray_march<1, 1024>
-                         : mode == 2 ? (const void*)k_ray_march<2, 1024> : (const void*)k_ray_march<0, 1024>;
-    return mode == 1 ? (const void*)k_ray_march<1, 512>
-                     : mode == 2 ? (const void*)k_ray_march<2, 512> : (const void*)k_ray_march<0, 512>;
+static const void* ray_kernel(int mode, int nt, bool fast) {
+    if (fast) {
+        if (nt == 640)
+            return mode == 1 ? (const void*)k_ray_march<1, 640, 1>
+                             : mode == 2 ? (const void*)k_ray_march<2, 640, 1> : (const void*)k_ray_march<0, 640, 1>;
+        return mode == 1 ? (const void*)k_ray_march<1, 512, 1>
+                         : mode == 2 ? (const void*)k_ray_march<2, 512, 1> : (const void*)k_ray_march<0, 512, 1>;
+    }
+    return mode == 1 ? (const void*)k_ray_march<1, 512, 0>
+                     : mode == 2 ? (const void*)k_ray_march<2, 512, 0> : (const void*)k_ray_march<0, 512, 0>;
 }
 
 // nt: threads per CTA (one CTA per SM); max_skip: see advance_impl
@@ -413,8 +425,9 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     if (off + 16 + cells * 4 <= kSmemMax) cfg.sm_mu = take((int)cells * 4);
     else if (p.adv.skip_empty && off + 16 + ((cells + 31) >> 5) * 4 <= kSmemMax)
         cfg.sm_occ = take((int)(((cells + 31) >> 5) * 4));
-    if (mode == 2) nt = 512;
-    const void* fn = ray_kernel(mode, nt);
+    const bool fast = cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty;
+    if (mode == 2 || !fast) nt = 512;
+    const void* fn = ray_kernel(mode, nt, fast);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, off);

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 from conftest import load_golden  # noqa: E402
 from oracle_runner import oracle_state, record_array, run_oracle_session  # noqa: E402
 
-THROUGHPUT = [10, 11, 13, 14]
+THROUGHPUT = [10, 11, 12, 14]
 
 
 @pytest.fixture(scope="module", autouse=True)
