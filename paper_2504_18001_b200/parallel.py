@@ -131,6 +131,96 @@ class FusedGather:
         return self.local
 
 
+def interleave_bands(bands: torch.Tensor, height: int) -> torch.Tensor:
+    """(world, per, W, C) padded bands -> the (height, W, C) frame: band r's row j is
+    film row r + j*world."""
+    world, per = bands.shape[0], bands.shape[1]
+    return bands.transpose(0, 1).reshape(per * world, *bands.shape[2:])[:height]
+
+
+def gather_bands_to_root(ctx: Ctx, band: torch.Tensor, height: int, out: torch.Tensor = None):
+    """Gather every rank's interleaved row band (padded to ceil(height/world) rows) to
+    rank 0; returns the assembled frame on rank 0, None elsewhere.  NCCL on CUDA
+    tensors, gloo on host tensors (the CPU tests)."""
+    if ctx.world == 1:
+        return band
+    per = -(-height // ctx.world)
+    if band.shape[0] != per:
+        pad = torch.zeros((per,) + tuple(band.shape[1:]), dtype=band.dtype, device=band.device)
+        pad[: band.shape[0]] = band
+        band = pad
+    if ctx.rank == 0:
+        if out is None:
+            out = torch.empty((ctx.world,) + tuple(band.shape), dtype=band.dtype, device=band.device)
+        dist.gather(band, gather_list=list(out.unbind(0)), dst=0)
+        return interleave_bands(out, height)
+    dist.gather(band, gather_list=None, dst=0)
+    return None
+
+
+class FrameGather:
+    """Frame assembly for N>1 on a comm stream that overlaps the next frame.
+
+    Sort-first tiles: each rank quantises its film-row band to RGBA8 on the render
+    stream (vcb_frame_rgba8 = image_io.to_rgba8, 4 B/pixel instead of 16), then the
+    comm stream waits for it and NCCL-gathers the bands to rank 0 while the render
+    stream goes on with the next frame.  Alternate-frame rendering gathers whole
+    RGBA8 frames the same way.  Two band buffers per rank; the render stream only
+    reuses one after the gather that read it has finished."""
+
+    def __init__(self, ctx: Ctx, sess, height: int, width: int, frames: bool = False):
+        from . import _native as N
+        from .device import ptr, stream_ptr
+
+        self.N, self.ptr, self.stream_ptr = N, ptr, stream_ptr
+        self.ctx, self.sess, self.H, self.W, self.frames = ctx, sess, height, width, frames
+        dev = torch.device("cuda", ctx.local_rank)
+        self.rows = height if frames else -(-height // ctx.world)
+        self.comm = torch.cuda.Stream(dev)
+        self.bands = [torch.zeros((self.rows, width, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.done = [None, None]
+        self.out = [torch.empty((ctx.world, self.rows, width, 4), dtype=torch.uint8, device=dev)
+                    for _ in range(2)] if ctx.rank == 0 else None
+        self.i = 0
+        self.last = None
+
+    def submit(self, img: torch.Tensor):
+        """Queue this rank's part of the current frame (img: f32 (rows, W, 4))."""
+        k = self.i % 2
+        st = self.sess.stream
+        if self.done[k] is not None:
+            st.wait_event(self.done[k])
+        with torch.cuda.stream(st):
+            self.N.call("vcb_frame_rgba8", self.ptr(img), img.numel() // 4, self.ptr(self.bands[k]),
+                        self.stream_ptr(st))
+        ready = torch.cuda.Event()
+        ready.record(st)
+        self.comm.wait_event(ready)
+        with torch.cuda.stream(self.comm):
+            if self.ctx.world > 1:
+                dist.gather(self.bands[k], gather_list=list(self.out[k].unbind(0)) if self.ctx.rank == 0 else None,
+                            dst=0)
+            ev = torch.cuda.Event()
+            ev.record(self.comm)
+        self.done[k] = ev
+        self.last = k
+        self.i += 1
+
+    def drain(self):
+        self.comm.synchronize()
+
+    def host_frame(self):
+        """Rank 0: the last submitted frame(s) as host RGBA8 (H, W, 4), or (world, H, W, 4)
+        for alternate-frame rendering."""
+        self.comm.synchronize()
+        o = self.out[self.last]
+        full = o if self.frames else interleave_bands(o, self.H)
+        return full.cpu().numpy()
+
+    def close(self):
+        self.drain()
+
+
 def barrier(ctx: Ctx):
     if ctx.world > 1:
         dist.barrier()

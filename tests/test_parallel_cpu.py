@@ -65,3 +65,56 @@ def test_rows_partition_is_exact_cover():
         for world in (1, 2, 4, 8):
             rows = sorted(r for k in range(world) for r in parallel.rows_of(k, world, H))
             assert rows == list(range(H))
+
+
+def _root_worker(rank, world, port, H, W, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from paper_2504_18001_b200 import parallel
+
+    ctx = parallel.init_from_env(backend="gloo")
+    rows = parallel.rows_of(rank, world, H)
+    # RGBA8 band (the FrameGather payload): film row r carries (r, column, rank, 255)
+    band = torch.tensor([[[r, c, rank, 255] for c in range(W)] for r in rows], dtype=torch.uint8)
+    full = parallel.gather_bands_to_root(ctx, band, H)
+    q.put((rank, None if full is None else full.numpy()))
+    parallel.shutdown(ctx)
+
+
+@pytest.mark.parametrize("H,world", [(7, 2), (9, 3)])
+def test_rgba8_bands_gather_to_rank0(H, world):
+    """Sort-first frame assembly (FrameGather's gather + interleave) over gloo."""
+    W = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_root_worker, args=(r, world, port, H, W, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(1, world):
+        assert res[r] is None
+    full = res[0]
+    assert full.shape == (H, W, 4)
+    np.testing.assert_array_equal(full[..., 0], np.repeat(np.arange(H)[:, None], W, axis=1))
+    np.testing.assert_array_equal(full[..., 1], np.repeat(np.arange(W)[None, :], H, axis=0))
+    np.testing.assert_array_equal(full[..., 2], np.repeat((np.arange(H) % world)[:, None], W, axis=1))
+
+
+def test_interleave_bands_matches_rows_of():
+    from paper_2504_18001_b200 import parallel
+
+    H, world, W = 11, 4, 3
+    per = -(-H // world)
+    bands = torch.full((world, per, W, 1), -1.0)
+    for r in range(world):
+        for j, row in enumerate(parallel.rows_of(r, world, H)):
+            bands[r, j] = row
+    full = parallel.interleave_bands(bands, H)
+    np.testing.assert_array_equal(full[:, 0, 0].numpy(), np.arange(H))
