@@ -81,6 +81,15 @@ SESSION_SPECS = {
         brick=16, pool=(4, 4, 4), policy=dict(lod_scale=1.2, preload_frames=20),
         res=(64, 64), frames=12, cam_step=10,
     ),
+    # BASELINE config 1 at its stated size: 64^3 random-init INR, B16, the 2-level paged
+    # MRPD (test_cache.py:184-200 knobs), 4^3 pool, 256x256, the full 120-frame orbit,
+    # warm_body(0.5, 0.9), LodPolicy(1.2, preload 20), 40 requests/frame
+    # (images kept every 20th frame: tests/golden/make_config1.py)
+    "config1": dict(
+        field="inr", dims=(64, 64, 64), tf=("warm_body", 0.5, 0.9),
+        brick=16, pool=(4, 4, 4), cache_kw=dict(direct_table_threshold=8, page_size=4, page_budget=2),
+        policy=dict(lod_scale=1.2, preload_frames=20), res=(256, 256), frames=120, cam_step=1,
+    ),
     # uncached INR baseline (every sample inferred; session.py:63-70)
     "inr_uncached": dict(
         field="inr", dims=(32, 32, 32), tf=("warm_body", 0.5, 0.9), cached=False,
