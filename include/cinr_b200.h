@@ -193,6 +193,10 @@ typedef struct {
     int64_t workspace_bytes;
     int64_t *dbg_reports;    /* optional [total][2] (flat id, count), NULL to skip */
     VcbField field;
+    const int64_t *frame_nonfinite;  /* optional device flag (VcbFrameStats.nonfinite of the frame just
+                                        rendered): when set the whole maintenance is skipped on the device,
+                                        as the reference raises RenderError before _maintenance runs
+                                        (sampler.py:149-152, session.py:107-112) */
 } VcbMaintParams;
 
 /* Path tracing (render/pathtrace.py:112-146, session.py:108-109): samples_per_pixel
@@ -225,8 +229,9 @@ typedef struct {
     int64_t batch, steps, step0;   /* step0 = optimizer steps already taken (Adam t) */
     int32_t optimizer;             /* 0 = Adam (train.py:51-75), 1 = SGD (40-48), 2 = none (lr 0) */
     int32_t flags;                 /* bit 0: pos/targets given by the caller (no PCG batch, no decode);
-                                      bit 1: keep the gradients (loss_and_grads, train.py:16-37: no update) */
-    double lr, beta1, beta2, eps, clip_norm;   /* clip_norm <= 0: no clipping (78-85) */
+                                      bit 1: keep the gradients (loss_and_grads, train.py:16-37: no update);
+                                      bit 2: clip by the global norm clip_norm (train.py:78-85; unset = None) */
+    double lr, beta1, beta2, eps, clip_norm;
     uint64_t pcg_state[2], pcg_inc[2];
     uint64_t draw0;
     int64_t n_table_params, n_weights, n_params;  /* flat parameter order: tables, weights, biases */

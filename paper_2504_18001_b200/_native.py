@@ -92,7 +92,8 @@ class VcbMaintParams(C.Structure):
                 ("max_requests", i32), ("ranking", i32), ("rank_clamp", i64), ("lin_bits", i32), ("lod_bits", i32),
                 ("table", vp), ("pool", vp), ("owner", vp), ("last_used", vp), ("miss_count", vp),
                 ("req_base", vp), ("req_hits", vp), ("state", vp), ("staging", vp), ("staged_keys", vp),
-                ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField)]
+                ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField),
+                ("frame_nonfinite", vp)]
 
 
 class VcbPtParams(C.Structure):
@@ -157,13 +158,28 @@ def load():
     if _LIB is not None:
         return _LIB
     try:
+        import fcntl
+
         from . import _build
 
         if _build.needs_build():
-            _build.build()
-    except Exception as exc:  # a missing nvcc on a prebuilt tree is fine
+            # one builder at a time (torchrun ranks share the tree); the others wait and
+            # then find the library current
+            _build.OUT_DIR.mkdir(exist_ok=True)
+            with open(_build.OUT_DIR / ".build.lock", "w") as lk:
+                fcntl.flock(lk, fcntl.LOCK_EX)
+                try:
+                    if _build.needs_build():
+                        _build.build()
+                finally:
+                    fcntl.flock(lk, fcntl.LOCK_UN)
+    except Exception as exc:
         if not _SO.exists():
             raise NativeUnavailable(f"cannot build {_SO.name}: {exc}") from exc
+        # a prebuilt library without a toolchain is fine; a failed rebuild of changed
+        # sources is not (the stale library would not match them)
+        if "nvcc not found" not in str(exc):
+            raise NativeUnavailable(f"rebuild of {_SO.name} failed: {exc}") from exc
     if not _SO.exists():
         raise NativeUnavailable(f"{_SO} not built (run __graft_entry__.build())")
     try:
@@ -174,8 +190,20 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    _check_abi(lib)
     _LIB = lib
     return lib
+
+
+def _check_abi(lib):
+    """ctypes mirrors vs the library's struct sizes, on every load."""
+    import numpy as np
+
+    out = np.zeros(16, dtype=np.int64)
+    n = lib.vcb_struct_sizes(out.ctypes.data, 16)
+    bad = [(s.__name__, C.sizeof(s), int(out[i])) for i, s in enumerate(STRUCTS[:n]) if C.sizeof(s) != int(out[i])]
+    if bad:
+        raise NativeUnavailable(f"{_SO.name} ABI mismatch (python, C sizeof): {bad}")
 
 
 STRUCTS = (VcbCamera, VcbMarchStatic, VcbProbeStatic, VcbField, VcbBrickGeom, VcbFrameStats, VcbCacheState,

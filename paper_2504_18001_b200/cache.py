@@ -243,7 +243,7 @@ class DeviceCache:
         self.req_hits.zero_()
         self.state.zero_()
 
-    def maint_params(self, session_frame: int, field_desc) -> N.VcbMaintParams:
+    def maint_params(self, session_frame: int, field_desc, skip_flag=None) -> N.VcbMaintParams:
         p = N.VcbMaintParams()
         p.geom = self.geom
         p.total = self.layout.total
@@ -268,10 +268,13 @@ class DeviceCache:
         p.workspace_bytes = self.workspace.numel()
         p.dbg_reports = ptr(self.dbg_reports)
         p.field = field_desc
+        p.frame_nonfinite = skip_flag
         return p
 
-    def maintenance(self, session_frame: int, field_desc, stream=None):
-        p = self.maint_params(session_frame, field_desc)
+    def maintenance(self, session_frame: int, field_desc, stream=None, skip_flag=None):
+        """vcb_maintenance; skip_flag = device address of the frame's non-finite flag
+        (the maintenance then skips itself on the device when the frame failed)."""
+        p = self.maint_params(session_frame, field_desc, skip_flag)
         N.call("vcb_maintenance", C.byref(p), stream_ptr(stream))
 
     # ---- diagnostics (D2H; not on the hot path)

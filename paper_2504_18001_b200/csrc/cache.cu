@@ -31,8 +31,13 @@ struct MaintWs {
     int* ctr;              // [0] n_pending, [1] n_reports
     long long* lru;        // [kMaxSel]
     int* assign;           // [kMaxSel]
-    int* nonfinite;
+    int* nonfinite;        // [0] decode flag, [1] skip (the frame failed), [2..3] bricks to decode (i64)
+    __host__ __device__ long long* n_dec() const { return reinterpret_cast<long long*>(nonfinite + 2); }
 };
+
+// The frame just rendered raised a non-finite inference: the reference raises
+// RenderError before _maintenance (sampler.py:149-152), so nothing here may run.
+__device__ __forceinline__ bool maint_skipped(const MaintWs& w) { return w.nonfinite[1] != 0; }
 
 inline int64_t maint_ws_layout(int64_t total, void* base, MaintWs* w) {
     size_t off = 0;
@@ -61,7 +66,14 @@ __device__ __forceinline__ int lod_of(const VcbBrickGeom& G, long long flat) {
     return lod;
 }
 
+__global__ void k_maint_gate(VcbMaintParams P, MaintWs w) {
+    w.nonfinite[0] = 0;
+    w.nonfinite[1] = (P.frame_nonfinite != nullptr && *P.frame_nonfinite != 0) ? 1 : 0;
+    *w.n_dec() = 0;
+}
+
 __global__ void k_report(VcbMaintParams P, MaintWs w) {
+    if (maint_skipped(w)) return;
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
          b += (long long)gridDim.x * blockDim.x) {
         const int c = P.miss_count[b];
@@ -174,6 +186,7 @@ __device__ int block_select_smallest(KeyFn key_of, long long n, int m, SelSmem& 
 __global__ void __launch_bounds__(kSelThreads) k_insert(VcbMaintParams P, MaintWs w) {
     __shared__ SelSmem s;
     __shared__ long long n_lru_s;
+    if (maint_skipped(w)) return;
     VcbCacheState* st = P.state;
     const long long n = st->n_staged;
     if (n == 0) {
@@ -277,6 +290,7 @@ __device__ __forceinline__ unsigned long long composite_key(const VcbMaintParams
 }
 
 __global__ void k_pending(VcbMaintParams P, MaintWs w) {
+    if (maint_skipped(w)) return;
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
          b += (long long)gridDim.x * blockDim.x) {
         if (P.req_base[b] < 0) continue;
@@ -291,6 +305,7 @@ __global__ void k_pending(VcbMaintParams P, MaintWs w) {
 __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintWs w) {
     __shared__ SelSmem s;
     __shared__ long long picked[kMaxSel];
+    if (maint_skipped(w)) return;
     VcbCacheState* st = P.state;
     const long long np = w.ctr[0];
     const int m = P.max_requests < kMaxSel ? P.max_requests : kMaxSel;
@@ -315,6 +330,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
         P.staged_keys[i] = P.geom.offset[lod] + lin;
     }
     if (threadIdx.x == 0) {
+        *w.n_dec() = cnt;
         st->n_staged = cnt;
         st->staged_frame = P.session_frame;
         st->n_inflight = cnt;
@@ -363,6 +379,7 @@ __global__ void k_decode_bricks_dev(VcbField F, VcbBrickGeom G, const int64_t* k
 }
 
 __global__ void k_post_decode(VcbMaintParams P, MaintWs w) {
+    if (maint_skipped(w)) return;
     VcbCacheState* st = P.state;
     if (*w.nonfinite) {
         // InlineLoader.dispatch failure: keys re-enter with base = f, hits = 0
@@ -401,8 +418,9 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     if (need > P.workspace_bytes) return set_error("maintenance: workspace too small");
     cudaMemsetAsync(w.ctr, 0, 64, st);
     // the decode flag is per maintenance (set by this call's decode, read by k_post_decode);
-    // the workspace comes uninitialised from the caller
-    cudaMemsetAsync(w.nonfinite, 0, 4, st);
+    // the workspace comes uninitialised from the caller.  The gate also reads the frame's
+    // non-finite flag: a failed frame skips every step below on the device.
+    k_maint_gate<<<1, 1, 0, st>>>(P, w);
     const int g = grid_for(P.total, 256, 8);
     // 1. drain miss reports into the request table (session.py:135-136)
     k_report<<<g, 256, 0, st>>>(P, w);
@@ -415,7 +433,7 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     const int sm = mlp_smem_bytes(P.field);
     const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
     const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
-    const int64_t* nst = (const int64_t*)((char*)P.state + offsetof(VcbCacheState, n_staged));
+    const int64_t* nst = (const int64_t*)w.n_dec();  // the batch k_select staged (0 when skipped)
     if (P.field.kind == 0 && inr_is_default(P.field)) {
         // the default INR decodes on the tensor cores (tcgen05, decode_tc.cu)
         inr_bricks_tc_dev(P.field, P.geom, P.staged_keys, nst, P.max_requests, P.staging, w.nonfinite, st);
@@ -424,6 +442,6 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
                           P.max_requests, P.staging, w.nonfinite);
     }
     k_post_decode<<<1, 1, 0, st>>>(P, w);
-    g_launches += 6;
+    g_launches += 7;
     return check_launch("maintenance");
 }

@@ -55,7 +55,12 @@ __device__ __forceinline__ double tr_pcg_out(u128 s) {
 }
 
 // pos[i][a] = draw (draw0 + step*3B + 3i + a)
+// P.scratch[1] != 0: an earlier step's loss was non-finite (k_tr_after); the run has
+// diverged and every later step's kernels return at once (train.py:123-127 stops there).
+__device__ __forceinline__ bool tr_diverged(const VcbTrainParams& P) { return P.scratch[1] != 0.0; }
+
 __global__ void k_tr_positions(VcbTrainParams P, long long step) {
+    if (tr_diverged(P)) return;
     const TrJump* J = reinterpret_cast<const TrJump*>(P.jump);
     const u128 A = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
     const u128 inc = ((u128)P.pcg_inc[1] << 64) | P.pcg_inc[0];
@@ -91,6 +96,7 @@ struct TrSmem {
 template <bool kSig>
 __global__ void __launch_bounds__(kTrB, 5) k_tr_step(VcbTrainParams P, long long step) {
     extern __shared__ __align__(16) unsigned char tr_smem[];
+    if (tr_diverged(P)) return;
     TrSmem& S = *reinterpret_cast<TrSmem*>(tr_smem);
     const VcbField& F = P.model;
     const float* W0 = F.weights + F.w_off[0];  // [32][16]
@@ -273,6 +279,7 @@ __device__ __forceinline__ float* tr_param(const VcbTrainParams& P, long long q)
 
 // train.py:81: sum of the f32 gradients squared, in f64
 __global__ void k_tr_gnorm(VcbTrainParams P) {
+    if (tr_diverged(P)) return;
     double s = 0.0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < P.n_params;
          q += (long long)gridDim.x * blockDim.x) {
@@ -289,7 +296,7 @@ __global__ void k_tr_update(VcbTrainParams P, long long step, double bc1, double
     const bool stop = !isfinite(ls) || P.scratch[1] != 0.0 || P.optimizer == 2;  // 2: learning rate 0
     float scale = 1.0f;
     bool clip = false;
-    if (P.clip_norm > 0.0) {
+    if (P.flags & 4) {  // clip_norm given (None = no clipping; 0 zeroes the gradients, train.py:78-85)
         const double total = sqrt(P.scratch[0]);
         if (!(total <= P.clip_norm || total == 0.0)) {
             clip = true;
@@ -363,12 +370,12 @@ extern "C" int32_t vcb_train_steps(const VcbTrainParams* pp, void* stream_) {
             launches += 1;
             continue;  // loss_and_grads: gradients stay in P.grads
         }
-        if (P.clip_norm > 0.0) k_tr_gnorm<<<gu, 256, 0, st>>>(P);
+        if (P.flags & 4) k_tr_gnorm<<<gu, 256, 0, st>>>(P);
         const double t = (double)(P.step0 + s + 1);
         const double bc1 = 1.0 - std::pow(P.beta1, t), bc2 = 1.0 - std::pow(P.beta2, t);
         k_tr_update<<<gu, 256, 0, st>>>(P, s, bc1, bc2);
         k_tr_after<<<1, 1, 0, st>>>(P, s);
-        launches += 5 + (P.clip_norm > 0.0 ? 1 : 0);
+        launches += 5 + ((P.flags & 4) ? 1 : 0);
     }
     return check_launch("train_steps");
 }

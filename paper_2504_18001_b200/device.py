@@ -87,12 +87,34 @@ def _inr_desc(model_like, device, clip):
     return DeviceField(d, (tab, wt, bt))
 
 
+def _param_fingerprint(model):
+    """Content fingerprint of an INR's parameters (1.4 MB for the default model, a CRC
+    in well under a millisecond): in-place edits (the reference's optimizers update
+    arrays in place, users may write model.tables[i][:]) invalidate the cached copy."""
+    import zlib
+
+    crc = 0
+    for a in getattr(model, "parameters", lambda: [])():
+        a = np.ascontiguousarray(a)
+        crc = zlib.crc32(a.view(np.uint8).reshape(-1), crc)
+        crc = zlib.crc32(repr((a.shape, a.dtype.str)).encode(), crc)
+    return ("inr", crc)
+
+
+def _lattice_identity(field_src):
+    """Lattices can be GBs: keyed on the array's identity and data address (a lattice
+    edited in place needs a new field object)."""
+    lat = getattr(field_src, "lattice", None)
+    if lat is None:
+        return ("other", id(field_src))
+    return ("lattice", id(lat), lat.__array_interface__["data"][0], lat.shape)
+
+
 def device_field(field_src, device=None, clip=True) -> DeviceField:
     """Descriptor for this package's fields or the reference's (duck typed)."""
     dev = require_cuda(device)
     model = getattr(field_src, "model", None)
-    version = getattr(model, "_version", 0) if model is not None else 0
-    key = (str(dev), clip, version, id(getattr(model, "tables", None)) if model is not None else 0)
+    key = (str(dev), clip, _param_fingerprint(model) if model is not None else _lattice_identity(field_src))
     cache = getattr(field_src, "_cinr_dev", None)
     if cache is not None and cache[0] == key:
         return cache[1]

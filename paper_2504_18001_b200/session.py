@@ -102,6 +102,7 @@ class RenderSession:
         self._ws = None
         self._img = None
         self._stats = torch.zeros(C.sizeof(N.VcbFrameStats) // 8, dtype=torch.int64, device=self.device)
+        self._nonfinite_off = N.VcbFrameStats.nonfinite.offset
         self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
@@ -166,8 +167,9 @@ class RenderSession:
             self._mu = torch.empty(self._vminmax[0].shape, dtype=torch.float32, device=self.device)
         bm = torch.from_numpy(macrocell.opacity_bin_maxima(tf)).to(self.device)
         vmin, vmax = self._vminmax
-        N.call("vcb_update_majorants", ptr(vmin), ptr(vmax), vmin.numel(), ptr(bm), bm.numel(), ptr(self._mu),
-               stream_ptr(self.stream))
+        with torch.cuda.device(self.device):  # the session stream's device, whatever is current
+            N.call("vcb_update_majorants", ptr(vmin), ptr(vmax), vmin.numel(), ptr(bm), bm.numel(), ptr(self._mu),
+                   stream_ptr(self.stream))
         self._bm = bm  # keep alive until the stream ran
         self._lut = torch.from_numpy(np.ascontiguousarray(tf.lookup_table(), dtype=np.float32)).to(self.device)
         # control points for the path tracer's np.interp (tf.opacity / tf.eval, transfer.py:28-56)
@@ -349,7 +351,10 @@ class RenderSession:
             else:
                 N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
             if self.cache is not None:
-                self.cache.maintenance(self.frame, self._dfield.desc, self.stream)
+                # a frame whose true-miss inference failed raises RenderError in collect_record
+                # without advancing the clocks; its maintenance skips itself on the device
+                self.cache.maintenance(self.frame, self._dfield.desc, self.stream,
+                                       skip_flag=ptr(self._stats) + self._nonfinite_off)
             # one small D2H for the FrameRecord counters
             ns = self._stats.numel()
             self._host_stats[:ns].copy_(self._stats, non_blocking=True)

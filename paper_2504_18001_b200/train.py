@@ -44,6 +44,9 @@ def train(model, field_src, steps: int, batch_size: int = DEFAULT_BATCH_SIZE, le
     g, mc = model.grid_config, model.mlp_config
     if (g.levels, g.features_per_entry, mc.hidden_width, mc.hidden_layers) != (8, 2, 32, 2):
         raise ConfigError("the GPU trainer supports the default 8x2 hash grid + 16-32-32-1 MLP")
+    if np.dtype(getattr(model, "dtype", np.float32)) != np.float32:
+        # the reference updates parameters in the model's dtype; the device trainer is f32
+        raise ConfigError(f"the GPU trainer needs a float32 model (got {np.dtype(model.dtype)})")
     dev = require_cuda(device)
     df = _inr_desc(model, dev, clip=False)
     tab, wt, bt = df._keep
@@ -67,6 +70,7 @@ def train(model, field_src, steps: int, batch_size: int = DEFAULT_BATCH_SIZE, le
     p.optimizer = 2 if learning_rate == 0.0 else (0 if optimizer == "adam" else 1)
     p.lr, p.beta1, p.beta2, p.eps = float(learning_rate), 0.9, 0.999, 1e-9
     p.clip_norm = float(clip_norm) if clip_norm is not None else 0.0
+    p.flags = 4 if clip_norm is not None else 0
     p.pcg_state[0], p.pcg_state[1] = st & MASK64, st >> 64
     p.pcg_inc[0], p.pcg_inc[1] = inc & MASK64, inc >> 64
     p.draw0 = 0
@@ -75,7 +79,8 @@ def train(model, field_src, steps: int, batch_size: int = DEFAULT_BATCH_SIZE, le
     p.pos, p.targets, p.loss, p.scratch, p.nonfinite, p.jump = (ptr(pos), ptr(targets), ptr(loss), ptr(scratch),
                                                                  ptr(nonfinite), ptr(jump))
     stream = torch.cuda.current_stream(dev)
-    N.call("vcb_train_steps", C.byref(p), C.c_void_p(stream.cuda_stream))
+    with torch.cuda.device(dev):
+        N.call("vcb_train_steps", C.byref(p), C.c_void_p(stream.cuda_stream))
     stream.synchronize()
     trace = loss.cpu().numpy() / B
     # parameters back into the model (tables split per level, like model.parameters())
@@ -135,7 +140,8 @@ def loss_and_grads(model, positions, targets, device=None):
     p.pos, p.targets, p.loss, p.scratch, p.nonfinite, p.jump = (ptr(dpos), ptr(dtg), ptr(loss), ptr(scratch),
                                                                  ptr(nonfinite), ptr(jump))
     stream = torch.cuda.current_stream(dev)
-    N.call("vcb_train_steps", C.byref(p), C.c_void_p(stream.cuda_stream))
+    with torch.cuda.device(dev):
+        N.call("vcb_train_steps", C.byref(p), C.c_void_p(stream.cuda_stream))
     stream.synchronize()
     gh = grads.cpu().numpy().astype(model.dtype)
     out, o = [], 0

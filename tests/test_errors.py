@@ -61,6 +61,40 @@ def test_failed_miss_inference_in_a_frame_raises_render_error():
     macro = MacroCellGrid(16, (32, 32, 32), (2, 2, 2), grid, grid + 1.0, np.ones_like(grid))
     cfg = SessionConfig(cached=True, loader="inline", cache=P.CacheConfig(brick_size=16, pool_dims=(2, 2, 2)),
                         policy=P.LodPolicy(1.0, 2), seed=0)
-    sess = RenderSession(_nan_model().as_field(), P.warm_body(0.3, 0.9), traj.camera_at(0), cfg, macro=macro)
-    with pytest.raises(RenderError):
-        sess.render_frame()  # frame 0: every sample is a true miss
+    sess = RenderSession(_nan_model().as_field(), P.warm_body(0.3, 0.9), traj.camera_at(0), cfg, macro=macro,
+                         debug=True)
+    for attempt in range(2):
+        with pytest.raises(RenderError):
+            sess.render_frame()  # frame 0: every sample is a true miss
+        # the reference raises before _maintenance (sampler.py:149-152, session.py:107-112):
+        # neither clock advanced, no miss report was drained into the request table, no
+        # batch was dispatched, nothing was inserted
+        assert sess.frame == 0 and sess.cache.frame == 0, attempt
+        st = sess.debug_state()
+        assert st["entries"].shape[0] == 0 and st["batch"].shape[0] == 0, attempt
+        assert (st["tables"] < 0).all() and (st["owner"] < 0).all(), attempt
+        assert int(sess.cache.miss_count.sum().item()) > 0  # the frame's reports wait, undrained
+
+
+def test_param_fingerprint_sees_in_place_edits():
+    """The device copy of a model is keyed on its parameters' content."""
+    import paper_2504_18001_b200 as P
+    from paper_2504_18001_b200.device import _param_fingerprint
+
+    m = P.InrModel(P.HashGridConfig(), P.MLPConfig(), P.FieldDomain((16, 16, 16)), seed=0)
+    a = _param_fingerprint(m)
+    assert _param_fingerprint(m) == a
+    m.tables[0][0, 0] += 1.0  # in place, same array object
+    assert _param_fingerprint(m) != a
+
+
+def test_trainer_rejects_non_float32_models():
+    import paper_2504_18001_b200 as P
+    from paper_2504_18001_b200.errors import ConfigError
+    from paper_2504_18001_b200.train import train
+
+    class F64Model:  # a reference InrModel built with dtype=np.float64 (duck typed)
+        grid_config, mlp_config, dtype = P.HashGridConfig(), P.MLPConfig(), np.dtype(np.float64)
+
+    with pytest.raises(ConfigError):
+        train(F64Model(), P.make_procedural("sphere", (16, 16, 16)), steps=1)
