@@ -116,7 +116,8 @@ typedef struct {
     int64_t iterations, rays;
     int64_t misses_resolved;
     int64_t nonfinite;      /* true-miss inference produced NaN/Inf (ModelCorruptError) */
-    int64_t pad_[8];
+    int64_t deferred_misses; /* true misses left undecoded by the frame's decode budget (not composited) */
+    int64_t pad_[7];
 } VcbFrameStats;
 
 /* Device-resident cache bookkeeping (pool free list, loader, counters). */
@@ -169,6 +170,8 @@ typedef struct {
     int32_t image_global;    /* 0: image is this session's band [rows][W][4]; 1: image is the whole
                                 frame [height][W][4] (possibly a peer GPU's buffer mapped over NVLink)
                                 and local row j lands on film row row0 + j*row_step */
+    int64_t miss_budget;     /* frame scheduler: true misses the frame may decode (sampler.py:276-279 is
+                                unbounded: -1); past it a true miss is filed but not composited */
 } VcbFrameParams;
 
 typedef struct {
@@ -193,10 +196,18 @@ typedef struct {
     int64_t workspace_bytes;
     int64_t *dbg_reports;    /* optional [total][2] (flat id, count), NULL to skip */
     VcbField field;
-    const int64_t *frame_nonfinite;  /* optional device flag (VcbFrameStats.nonfinite of the frame just
-                                        rendered): when set the whole maintenance is skipped on the device,
-                                        as the reference raises RenderError before _maintenance runs
-                                        (sampler.py:149-152, session.py:107-112) */
+    const VcbFrameStats *frame_stats; /* optional: the frame just rendered (device).  nonfinite set: the
+                                        whole maintenance is skipped on the device, as the reference raises
+                                        RenderError before _maintenance runs (sampler.py:149-152,
+                                        session.py:107-112).  misses_resolved: the decode budget's share
+                                        the frame already used */
+    int64_t decode_budget;   /* frame scheduler: samples decoded per frame (true misses + brick batch);
+                                -1 = unbounded (the reference: max_requests bricks, all misses).  The batch
+                                is min(max_requests, max(1, (budget - misses_resolved) / B^3)) bricks */
+    int32_t defer_decode;    /* 1: the batch is decoded by vcb_maint_decode (on another stream, overlapping
+                                the next frame; inserted at the next maintenance as InlineLoader /
+                                ThreadLoader collect() would); 0: decoded inside this call */
+    int32_t pad2_;
 } VcbMaintParams;
 
 /* Path tracing (render/pathtrace.py:112-146, session.py:108-109): samples_per_pixel
@@ -333,6 +344,10 @@ int32_t vcb_frame_counters(const void *workspace, int64_t max_rays, int32_t max_
 int64_t vcb_last_launch_count(void);
 int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots, int32_t max_requests);
 int32_t vcb_maintenance(const VcbMaintParams *p, void *stream);
+/* The decode (fulfill, scheduler.py:127-134) of the batch the last vcb_maintenance with
+ * defer_decode = 1 selected, on `stream`: the caller orders it after that maintenance
+ * and before the next one (events), so it overlaps the next frame's march. */
+int32_t vcb_maint_decode(const VcbMaintParams *p, void *stream);
 
 #ifdef __cplusplus
 }

@@ -69,7 +69,8 @@ class VcbBrickGeom(C.Structure):
 
 class VcbFrameStats(C.Structure):
     _fields_ = [("requests", i64), ("exact", i64), ("fallback", i64), ("miss", i64), ("iterations", i64),
-                ("rays", i64), ("misses_resolved", i64), ("nonfinite", i64), ("pad_", i64 * 8)]
+                ("rays", i64), ("misses_resolved", i64), ("nonfinite", i64), ("deferred_misses", i64),
+                ("pad_", i64 * 7)]
 
 
 class VcbCacheState(C.Structure):
@@ -84,7 +85,7 @@ class VcbFrameParams(C.Structure):
                 ("lut_size", i32), ("max_iterations", i32), ("epoch", C.c_uint32), ("timing", i32),
                 ("mu", vp), ("lut", vp), ("table", vp), ("pool", vp), ("last_used", vp), ("miss_count", vp),
                 ("field", VcbField), ("image", vp), ("stats", vp), ("workspace", vp), ("workspace_bytes", i64),
-                ("impl", i32), ("image_global", i32)]
+                ("impl", i32), ("image_global", i32), ("miss_budget", i64)]
 
 
 class VcbMaintParams(C.Structure):
@@ -93,7 +94,7 @@ class VcbMaintParams(C.Structure):
                 ("table", vp), ("pool", vp), ("owner", vp), ("last_used", vp), ("miss_count", vp),
                 ("req_base", vp), ("req_hits", vp), ("state", vp), ("staging", vp), ("staged_keys", vp),
                 ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField),
-                ("frame_nonfinite", vp)]
+                ("frame_stats", vp), ("decode_budget", i64), ("defer_decode", i32), ("pad2_", i32)]
 
 
 class VcbPtParams(C.Structure):
@@ -143,6 +144,7 @@ _PROTOS = {
     "vcb_frame_counters": (i32, [vp, i64, i32, vp]),
     "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
     "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
+    "vcb_maint_decode": (i32, [C.POINTER(VcbMaintParams), vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

@@ -243,7 +243,7 @@ class DeviceCache:
         self.req_hits.zero_()
         self.state.zero_()
 
-    def maint_params(self, session_frame: int, field_desc, skip_flag=None) -> N.VcbMaintParams:
+    def maint_params(self, session_frame: int, field_desc, frame_stats=None, defer_decode=False) -> N.VcbMaintParams:
         p = N.VcbMaintParams()
         p.geom = self.geom
         p.total = self.layout.total
@@ -268,14 +268,23 @@ class DeviceCache:
         p.workspace_bytes = self.workspace.numel()
         p.dbg_reports = ptr(self.dbg_reports)
         p.field = field_desc
-        p.frame_nonfinite = skip_flag
+        p.frame_stats = frame_stats
+        budget = getattr(self.sched, "decode_budget", None)
+        p.decode_budget = -1 if budget is None else int(budget)
+        p.defer_decode = 1 if defer_decode else 0
         return p
 
-    def maintenance(self, session_frame: int, field_desc, stream=None, skip_flag=None):
-        """vcb_maintenance; skip_flag = device address of the frame's non-finite flag
-        (the maintenance then skips itself on the device when the frame failed)."""
-        p = self.maint_params(session_frame, field_desc, skip_flag)
+    def maintenance(self, session_frame: int, field_desc, stream=None, frame_stats=None, defer_decode=False):
+        """vcb_maintenance.  frame_stats = device address of the frame's VcbFrameStats (a
+        failed frame then skips the maintenance on the device; the decode budget's share
+        the frame used).  defer_decode: the batch is left for decode() on another stream."""
+        p = self.maint_params(session_frame, field_desc, frame_stats, defer_decode)
+        self._last_params = p
         N.call("vcb_maintenance", C.byref(p), stream_ptr(stream))
+
+    def decode(self, stream):
+        """The deferred fulfill of the batch the last maintenance selected (vcb_maint_decode)."""
+        N.call("vcb_maint_decode", C.byref(self._last_params), stream_ptr(stream))
 
     # ---- diagnostics (D2H; not on the hot path)
     def state_dict(self):

@@ -68,7 +68,7 @@ __device__ __forceinline__ int lod_of(const VcbBrickGeom& G, long long flat) {
 
 __global__ void k_maint_gate(VcbMaintParams P, MaintWs w) {
     w.nonfinite[0] = 0;
-    w.nonfinite[1] = (P.frame_nonfinite != nullptr && *P.frame_nonfinite != 0) ? 1 : 0;
+    w.nonfinite[1] = (P.frame_stats != nullptr && P.frame_stats->nonfinite != 0) ? 1 : 0;
     *w.n_dec() = 0;
 }
 
@@ -308,7 +308,16 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
     if (maint_skipped(w)) return;
     VcbCacheState* st = P.state;
     const long long np = w.ctr[0];
-    const int m = P.max_requests < kMaxSel ? P.max_requests : kMaxSel;
+    int m = P.max_requests < kMaxSel ? P.max_requests : kMaxSel;
+    if (P.decode_budget >= 0) {
+        // frame scheduler: the frame's decoded true misses came first; the batch gets the
+        // rest of the per-frame sample budget, at least one brick so the cache progresses
+        const long long b3 = P.geom.b * P.geom.b * P.geom.b;
+        const long long used = P.frame_stats != nullptr ? P.frame_stats->misses_resolved : 0;
+        long long nb = (P.decode_budget - used) / b3;
+        if (nb < 1) nb = 1;
+        if (nb < m) m = (int)nb;
+    }
     auto key_ok = [&](long long i, unsigned long long& k) -> bool {
         const long long v = w.pend_key[i];
         if (v < 0) return false;  // excluded (mapped)
@@ -408,6 +417,23 @@ extern "C" int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots
     return maint_ws_layout(total_bricks, nullptr, nullptr);
 }
 
+// fulfill (scheduler.py:127-134) of the batch k_select staged (w.n_dec keys, 0 when the
+// maintenance was skipped) into the staging slab, then the failure path (k_post_decode)
+static void maint_decode(const VcbMaintParams& P, const MaintWs& w, cudaStream_t st) {
+    const int sm = mlp_smem_bytes(P.field);
+    const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
+    const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
+    const int64_t* nst = (const int64_t*)w.n_dec();
+    if (P.field.kind == 0 && inr_is_default(P.field)) {
+        // the default INR decodes on the tensor cores (tcgen05, decode_tc.cu)
+        inr_bricks_tc_dev(P.field, P.geom, P.staged_keys, nst, P.max_requests, P.staging, w.nonfinite, st);
+    } else {
+        CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
+                          P.max_requests, P.staging, w.nonfinite);
+    }
+    k_post_decode<<<1, 1, 0, st>>>(P, w);
+}
+
 extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     const VcbMaintParams& P = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
@@ -429,19 +455,19 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     // 3. dispatch: select the batch (session.py:141, scheduler.py:152-169)
     k_pending<<<g, 256, 0, st>>>(P, w);
     k_select<<<1, kSelThreads, 0, st>>>(P, w);
-    // 4. fulfill into the staging slab (inserted at the next maintenance)
-    const int sm = mlp_smem_bytes(P.field);
-    const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
-    const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
-    const int64_t* nst = (const int64_t*)w.n_dec();  // the batch k_select staged (0 when skipped)
-    if (P.field.kind == 0 && inr_is_default(P.field)) {
-        // the default INR decodes on the tensor cores (tcgen05, decode_tc.cu)
-        inr_bricks_tc_dev(P.field, P.geom, P.staged_keys, nst, P.max_requests, P.staging, w.nonfinite, st);
-    } else {
-        CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
-                          P.max_requests, P.staging, w.nonfinite);
-    }
-    k_post_decode<<<1, 1, 0, st>>>(P, w);
-    g_launches += 7;
+    // 4. fulfill into the staging slab (inserted at the next maintenance); deferred: the
+    //    caller runs vcb_maint_decode on its decode stream
+    if (!P.defer_decode) maint_decode(P, w, st);
+    g_launches += P.defer_decode ? 5 : 7;
     return check_launch("maintenance");
+}
+
+extern "C" int32_t vcb_maint_decode(const VcbMaintParams* pp, void* stream_) {
+    const VcbMaintParams& P = *pp;
+    MaintWs w;
+    int64_t need = maint_ws_layout(P.total, P.workspace, &w);
+    if (need > P.workspace_bytes) return set_error("maint_decode: workspace too small");
+    maint_decode(P, w, (cudaStream_t)stream_);
+    g_launches += 2;
+    return check_launch("maint_decode");
 }

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) k_ray_setup(const __grid_constant__ VcbFr
 }
 
 struct RmSmem {
-    unsigned long long cnt[5];  // exact, fallback, miss, samples, rays
+    unsigned long long cnt[7];  // exact, fallback, miss, samples, rays, decoded misses, deferred misses
     int max_k;
 };
 
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(NT, 1)
     } else if (kInr != 0 && cfg.sm_mlp >= 0) {
         stage_mlp(p.field, reinterpret_cast<float*>(dsm + cfg.sm_mlp), mlp);
     }
-    if (threadIdx.x < 5) sm.cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 7) sm.cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) sm.max_k = 0;
     __syncthreads();
     const float* lut = s_lut ? s_lut : p.lut;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NT, 1)
     long long cur = 0;       // cursor_f bits (adaptive) or cursor_k
     double cr = 0.0, cg = 0.0, cb = 0.0, tr = 1.0;
     uint32_t rs = 0u;
-    unsigned c_ex = 0, c_fb = 0, c_ms = 0, c_rays = 0;
+    unsigned c_ex = 0, c_fb = 0, c_ms = 0, c_rays = 0, c_res = 0, c_def = 0;
     unsigned long long c_smp = 0;
     int max_k = 0, bad = 0;
     const long long n_list = __ldcg(cfg.n_rays);
@@ -307,6 +307,24 @@ __global__ void __launch_bounds__(NT, 1)
             }
         }
 
+        // ---- frame scheduler: a true miss is decoded only within the frame's budget; past
+        // it the sample is filed (above) but not composited (p.miss_budget < 0: unbounded,
+        // sampler.py:276-279)
+        c_ms += needinf;
+        if (p.miss_budget >= 0) {
+            const unsigned nb = __ballot_sync(0xffffffffu, needinf);
+            if (nb) {
+                long long base = 0;
+                if (lane == __ffs(nb) - 1) base = atomicAdd((unsigned long long*)&ctr->pad[2], (unsigned long long)__popc(nb));
+                base = __shfl_sync(0xffffffffu, base, __ffs(nb) - 1);
+                if (needinf && base + __popc(nb & lt_mask) >= p.miss_budget) {
+                    needinf = 0;
+                    samp = 0;  // not composited
+                    c_def++;
+                }
+            }
+        }
+
         // ---- true-miss inference (sampler.py:276-279): clip(world, 0, nextafter(1, 0))
         if (kInr == 1) {
             if (__any_sync(0xffffffffu, needinf)) {
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(NT, 1)
             v = rm_infer_lane<kInr>(p.field, clampd(a.px, 0.0, hmax), clampd(a.py, 0.0, hmax),
                                     clampd(a.pz, 0.0, hmax), mlp, &bad);
         }
-        c_ms += needinf;
+        c_res += needinf;
 
         // ---- shade + early termination
         if (samp) {
@@ -347,6 +365,8 @@ __global__ void __launch_bounds__(NT, 1)
     const unsigned long long t_ms = warp_sum((unsigned long long)c_ms);
     const unsigned long long t_sm = warp_sum(c_smp);
     const unsigned long long t_ry = warp_sum((unsigned long long)c_rays);
+    const unsigned long long t_rs = warp_sum((unsigned long long)c_res);
+    const unsigned long long t_df = warp_sum((unsigned long long)c_def);
     int mk = max_k;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
@@ -356,6 +376,8 @@ __global__ void __launch_bounds__(NT, 1)
         atomicAdd(&sm.cnt[2], t_ms);
         atomicAdd(&sm.cnt[3], t_sm);
         atomicAdd(&sm.cnt[4], t_ry);
+        if (t_rs) atomicAdd(&sm.cnt[5], t_rs);
+        if (t_df) atomicAdd(&sm.cnt[6], t_df);
         atomicMax(&sm.max_k, mk);
     }
     __syncthreads();
@@ -364,7 +386,8 @@ __global__ void __launch_bounds__(NT, 1)
         atomicAdd((unsigned long long*)&S->exact, sm.cnt[0]);
         atomicAdd((unsigned long long*)&S->fallback, sm.cnt[1]);
         atomicAdd((unsigned long long*)&S->miss, sm.cnt[2]);
-        atomicAdd((unsigned long long*)&S->misses_resolved, sm.cnt[2]);
+        atomicAdd((unsigned long long*)&S->misses_resolved, sm.cnt[5]);
+        if (sm.cnt[6]) atomicAdd((unsigned long long*)&S->deferred_misses, sm.cnt[6]);
         atomicAdd((unsigned long long*)&S->requests, sm.cnt[3]);
         atomicAdd((unsigned long long*)&S->rays, sm.cnt[4]);
         // wavefront iterations the parity schedule runs: the longest ray's samples + 1

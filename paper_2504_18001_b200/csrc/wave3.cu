@@ -310,6 +310,26 @@ __device__ __forceinline__ void w3_count_next(int* gnx, int* snx, long long jb, 
     }
 }
 
+// Frame scheduler (VcbFrameParams.miss_budget): whether this lane's queued true miss
+// may be decoded (counted in misses_resolved) or is left undecoded and not composited
+// (deferred_misses).  Warp-aggregated; call with every lane of the warp.
+__device__ __forceinline__ bool w3_budget(const VcbFrameParams& p, const FrameWs& w, bool want) {
+    const unsigned nb = __ballot_sync(__activemask(), want);
+    if (!nb) return false;
+    const int lane = threadIdx.x & 31, leader = __ffs(nb) - 1;
+    unsigned long long base = 0;
+    if (p.miss_budget >= 0 && lane == leader)
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(&w.ctr->pad[2]), (unsigned long long)__popc(nb));
+    base = __shfl_sync(__activemask(), base, leader);
+    const bool ok = want && (p.miss_budget < 0 || (long long)(base + __popc(nb & ((1u << lane) - 1u))) < p.miss_budget);
+    const unsigned okb = __ballot_sync(__activemask(), ok);
+    if (lane == leader) {
+        if (okb) atomicAdd((unsigned long long*)&p.stats->misses_resolved, (unsigned long long)__popc(okb));
+        if (nb & ~okb) atomicAdd((unsigned long long*)&p.stats->deferred_misses, (unsigned long long)__popc(nb & ~okb));
+    }
+    return ok;
+}
+
 // One queued true miss of iteration k-1 (sampler.py:276-279): field inference at the
 // sample, shade, then the advance of iteration k into the same slot of S_k.  Out of
 // line, so the register-hungry inference does not raise the phase's register budget.
@@ -325,14 +345,17 @@ static __device__ __noinline__ void w3_miss_item(const VcbFrameParams& p, const 
     double cr = __ldcg(s.cr[b] + j), cg = __ldcg(s.cg[b] + j), cb = __ldcg(s.cb[b] + j), tr = __ldcg(s.tr[b] + j);
     const double dx = __ldg(w.ray_dir + 3 * id), dy = __ldg(w.ray_dir + 3 * id + 1), dz = __ldg(w.ray_dir + 3 * id + 2);
     const double px = DADD(c.ox, DMUL(dx, tmid)), py = DADD(c.oy, DMUL(dy, tmid)), pz = DADD(c.oz, DMUL(dz, tmid));
-    int bad = 0;
-    const float v = field_eval<kInr>(p.field, clampd(px, 0.0, hmax), clampd(py, 0.0, hmax), clampd(pz, 0.0, hmax),
-                                     mlp, &bad);
-    if (bad) w.ctr->nonfinite = 1;
-    const bool dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr,
-                                                 cg, cb, tr)
-                               : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term,
-                                                  cr, cg, cb, tr);
+    bool dead = false;
+    if (w3_budget(p, w, true)) {
+        int bad = 0;
+        const float v = field_eval<kInr>(p.field, clampd(px, 0.0, hmax), clampd(py, 0.0, hmax),
+                                         clampd(pz, 0.0, hmax), mlp, &bad);
+        if (bad) w.ctr->nonfinite = 1;
+        dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr, cg, cb,
+                                          tr)
+                        : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr, cg,
+                                           cb, tr);
+    }
     int f = 0;
     if (dead) {
         w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
@@ -377,14 +400,19 @@ static __device__ __noinline__ void w3_miss_warp(const VcbFrameParams& p, const 
         py = clampd(DADD(c.oy, DMUL(dy, tmid)), 0.0, hmax);
         pz = clampd(DADD(c.oz, DMUL(dz, tmid)), 0.0, hmax);
     }
-    float v = inr_warp_default(p.field, fr, px, py, pz);
+    const bool granted = w3_budget(p, w, active);
+    float v = 0.0f;
+    if (__any_sync(0xffffffffu, granted)) v = inr_warp_default(p.field, fr, px, py, pz);
     if (!active) return;
-    if (!isfinite(v)) w.ctr->nonfinite = 1;
-    if (p.field.clip01) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
-    const bool dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr,
-                                                 cg, cb, tr)
-                               : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term,
-                                                  cr, cg, cb, tr);
+    bool dead = false;
+    if (granted) {
+        if (!isfinite(v)) w.ctr->nonfinite = 1;
+        if (p.field.clip01) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+        dead = smem_lut ? shade_one<true>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr, cg, cb,
+                                          tr)
+                        : shade_one<false>(v, dt, lut, p.lut_size, p.adv.adaptive, p.adv.dt_base, p.term, cr, cg,
+                                           cb, tr);
+    }
     int f = 0;
     if (dead) {
         w3_retire(p, __ldg(w.ray_pix + id), cr, cg, cb, tr);
@@ -734,7 +762,6 @@ __global__ void __launch_bounds__(NT, 1)
         atomicAdd((unsigned long long*)&p.stats->exact, sm.cnt[0]);
         atomicAdd((unsigned long long*)&p.stats->fallback, sm.cnt[1]);
         atomicAdd((unsigned long long*)&p.stats->miss, sm.cnt[2]);
-        atomicAdd((unsigned long long*)&p.stats->misses_resolved, sm.cnt[2]);
         if (cta == 0) {
             p.stats->requests = req;
             p.stats->iterations = iters;

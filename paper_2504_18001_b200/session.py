@@ -102,7 +102,6 @@ class RenderSession:
         self._ws = None
         self._img = None
         self._stats = torch.zeros(C.sizeof(N.VcbFrameStats) // 8, dtype=torch.int64, device=self.device)
-        self._nonfinite_off = N.VcbFrameStats.nonfinite.offset
         self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
                                        dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
@@ -113,6 +112,11 @@ class RenderSession:
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
         self._target = None  # whole-frame buffer written in place (fused sort-first gather)
         self._pin_free = []  # pinned host frames released by callers
+        # loader="thread" (the reference's default, a background decode thread): the batch a
+        # maintenance selects is decoded on a decode stream while the next frame marches, and
+        # inserted by the next maintenance (the inline cadence, P12, so state is identical)
+        self._dstream = torch.cuda.Stream(self.device) if (config.loader == "thread" and config.cached) else None
+        self._ev_decoded = None
 
     MARCH_SCHEDULES = {"parity": 0, "throughput": 10}
 
@@ -190,8 +194,14 @@ class RenderSession:
             raise ValueError(f"unknown mode {mode!r}")
         self.mode = mode
 
+    def _sync_decode(self):
+        """Order the session stream after an outstanding deferred decode."""
+        if self._ev_decoded is not None:
+            self.stream.wait_event(self._ev_decoded)
+
     def reset_cache(self):
         if self.cache is not None:
+            self._sync_decode()
             with torch.cuda.stream(self.stream):
                 self.cache.reset()
         self.frame = 0
@@ -254,6 +264,8 @@ class RenderSession:
         p.field = self._dfield.desc
         p.image = ptr(image)
         p.image_global = 1 if (self._target is not None and image is self._target) else 0
+        budget = getattr(cfg.scheduler, "decode_budget", None)
+        p.miss_budget = -1 if budget is None else int(budget)
         p.stats = ptr(self._stats)
         need = N.load().vcb_frame_workspace_bytes(W * p.cam.rows, p.max_iterations)
         if self._ws is None or self._ws.numel() < need:
@@ -353,8 +365,17 @@ class RenderSession:
             if self.cache is not None:
                 # a frame whose true-miss inference failed raises RenderError in collect_record
                 # without advancing the clocks; its maintenance skips itself on the device
-                self.cache.maintenance(self.frame, self._dfield.desc, self.stream,
-                                       skip_flag=ptr(self._stats) + self._nonfinite_off)
+                if self._ev_decoded is not None:
+                    self.stream.wait_event(self._ev_decoded)  # the batch this maintenance inserts
+                self.cache.maintenance(self.frame, self._dfield.desc, self.stream, frame_stats=ptr(self._stats),
+                                       defer_decode=self._dstream is not None)
+                if self._dstream is not None:
+                    sel = torch.cuda.Event()
+                    sel.record(self.stream)
+                    self._dstream.wait_event(sel)
+                    self.cache.decode(self._dstream)
+                    self._ev_decoded = torch.cuda.Event()
+                    self._ev_decoded.record(self._dstream)
             # one small D2H for the FrameRecord counters
             ns = self._stats.numel()
             self._host_stats[:ns].copy_(self._stats, non_blocking=True)
@@ -471,6 +492,7 @@ class RenderSession:
     def export_state(self):
         """Full device state as host arrays (tables, pool, owners, stamps, requests,
         staged loader batch): lets another implementation resume this session."""
+        self._sync_decode()
         self.stream.synchronize()
         c = self.cache
         d = c.dump()
@@ -490,6 +512,7 @@ class RenderSession:
 
     def debug_state(self):
         """Reference-shaped per-frame state (tables, owner, stamps, requests, batch, reports)."""
+        self._sync_decode()
         self.stream.synchronize()
         d = self.cache.dump()
         d["batch"] = self.cache.batch()
@@ -497,6 +520,7 @@ class RenderSession:
         return d
 
     def close(self):
+        self._sync_decode()
         self.stream.synchronize()
 
     def __enter__(self):

@@ -38,7 +38,7 @@ def product_config(spec):
 
     return SessionConfig(
         cached=spec.get("cached", True), mode=spec.get("mode", "raymarch"), samples_per_pixel=spec.get("spp", 1),
-        loader="inline",
+        loader=spec.get("loader", "inline"),
         cache=P.CacheConfig(brick_size=spec["brick"], pool_dims=tuple(spec["pool"]), **spec.get("cache_kw", {})),
         scheduler=P.SchedulerConfig(**spec.get("sched_kw", {})), policy=P.LodPolicy(**spec["policy"]),
         settings=P.RenderSettings(**spec.get("settings", {})), seed=spec.get("seed", 0),
