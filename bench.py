@@ -372,6 +372,8 @@ def main():
     ap.add_argument("--config3-steps", type=int, default=10, help="config 3 (4096^3 virtual) timed frames (0 = skip)")
     ap.add_argument("--config3-preroll", type=int, default=60)
     ap.add_argument("--uncached-steps", type=int, default=5, help="frames of the no-cache INR baseline (0 = skip)")
+    ap.add_argument("--scheduler-frames", type=int, default=8, help="frame-scheduler cold-start frames (0 = skip)")
+    ap.add_argument("--budget", type=int, default=1 << 20, help="decode budget (samples/frame) of that comparison")
     ap.add_argument("--train-steps", type=int, default=50,
                     help="INR training steps at batch 65536 (inr/train.py on the GPU; 0 = skip)")
     ap.add_argument("--pt-steps", type=int, default=5,
@@ -531,6 +533,12 @@ def main():
                                    "last_samples": lr.samples}
             del s3
         torch.cuda.empty_cache()
+        # ---- frame scheduler: cold-start frames with and without a decode budget, and the
+        # overlapped (loader="thread") decode at steady state
+        if args.scheduler_frames > 0:
+            side["frame_scheduler"] = run_frame_scheduler(P, SessionConfig, parallel, ctx, fld, mg, traj, cam, args,
+                                                          flush, f_timed)
+            torch.cuda.empty_cache()
         # ---- config 3: 4096^3 virtual volume at 1024^2 (B=16, 10 LoD levels), steady state
         if args.config3_steps > 0:
             try:
@@ -629,6 +637,35 @@ def main():
     if gatherer is not None:
         gatherer.close()
     parallel.shutdown(ctx)
+
+
+def run_frame_scheduler(P, SessionConfig, parallel, ctx, fld, mg, traj, cam, args, flush, f_timed):
+    """The first frames of a cold session (every sample a true miss until the coarsest
+    brick lands at frame 2, P19) unbounded vs with SchedulerConfig(decode_budget), and
+    steady-state fps with loader='thread' (batch decoded on a side stream)."""
+    import dataclasses
+
+    out = {"budget_samples_per_frame": args.budget}
+    for label, budget in (("unbounded", None), ("budgeted", args.budget)):
+        cfg = session_config(P, SessionConfig)
+        cfg = dataclasses.replace(cfg, scheduler=dataclasses.replace(cfg.scheduler, decode_budget=budget))
+        s = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+        s.march = args.march
+        o = device_frames(s, cam, range(args.scheduler_frames), flush, s.stream)
+        st = [dict(ms=round(ms, 3), true_misses=r.true_misses) for ms, r in zip(o["ms"], o["recs"])]
+        out[label] = {"max_ms": max(o["ms"]), "mean_ms": statistics.mean(o["ms"]), "frames": st}
+        del s
+    cfg = dataclasses.replace(session_config(P, SessionConfig), loader="thread")
+    s = parallel.make_session(ctx, fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg)
+    s.march = args.march
+    preroll(s, cam, args.preroll + args.warmup)
+    o = device_frames(s, cam, range(f_timed, f_timed + args.steps), flush, s.stream)
+    out["thread_loader_steady_fps"] = len(o["ms"]) / (sum(o["ms"]) / 1000.0)
+    out["note"] = ("budgeted: true misses beyond the budget are filed but not composited, the brick batch gets what "
+                   "the misses left (>= 1 brick); thread loader: the batch decodes on a decode stream during the next "
+                   "frame's march (state identical to inline)")
+    del s
+    return out
 
 
 def run_config3(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev, peak, peak_src):
