@@ -129,7 +129,7 @@ __device__ __forceinline__ float mlp_2h(const float* feat, const MlpSmem& m, int
 
 // Any HashGridConfig/MLPConfig within the ABI limits (local-memory arrays).
 static __device__ __noinline__ float inr_generic(const VcbField& F, double x, double y, double z, const MlpSmem& m) {
-    float a[64], zv[64];
+    float a[128], zv[128];  // widths up to 128 (device.py checks)
     int k = 0;
     for (int l = 0; l < F.levels; l++) {
         const int nf = F.feats;

@@ -49,8 +49,10 @@ def _inr_desc(model_like, device, clip):
     m = model_like.mlp_config
     if g.levels > N.MAX_LEVELS:
         raise ConfigError(f"at most {N.MAX_LEVELS} hash-grid levels on the GPU path")
-    if g.levels * g.features_per_entry > 64 or m.hidden_width > 64 or m.hidden_layers + 1 > N.MAX_LAYERS:
-        raise ConfigError("MLP wider than 64 / deeper than 7 hidden layers is not supported on the GPU path")
+    if g.levels * g.features_per_entry > 128 or m.hidden_width > 128 or m.hidden_layers + 1 > N.MAX_LAYERS:
+        # the generic decoder keeps one activation row per thread (128 floats) and the
+        # weights in shared memory (width 128: 74 KB)
+        raise ConfigError("MLP wider than 128 / deeper than 7 hidden layers is not supported on the GPU path")
     tables = [np.asarray(t, dtype=np.float32) for t in model_like.tables]
     rows = [t.shape[0] for t in tables]
     tab = torch.from_numpy(np.ascontiguousarray(np.concatenate(tables, axis=0))).to(device)

@@ -127,6 +127,37 @@ def test_inr_decode_vs_reference():
     np.testing.assert_allclose(tiny.infer_batch(g["tiny_pos"]), g["tiny_infer"], atol=1e-5, rtol=0)
 
 
+@pytest.mark.parametrize("tag", ["w128", "w64x3"])
+def test_wide_inr_decode_vs_reference(tag):
+    """Wider MLPs than the default (the reference's MLPConfig.hidden_width is free):
+    width 128 x 2 and 64 x 3 hidden layers through the generic decoder and inside a
+    frame (true misses of an uncached session) against the reference's outputs."""
+    import paper_2504_18001_b200 as P
+
+    g = load_golden("inr_wide.npz")
+    mlp = (P.MLPConfig(hidden_width=128, hidden_layers=2) if tag == "w128"
+           else P.MLPConfig(hidden_width=64, hidden_layers=3, output_activation="clamp"))
+    m = P.InrModel(P.HashGridConfig(), mlp, P.FieldDomain((64, 64, 64)), seed=0)
+    r = np.random.default_rng(42)
+    m.set_parameters([r.uniform(-0.2, 0.2, size=p.shape).astype(np.float32) for p in m.parameters()])
+    pos = g[f"{tag}_pos"]
+    np.testing.assert_allclose(m.infer_batch(pos), g[f"{tag}_infer"], atol=1e-5, rtol=0)
+    np.testing.assert_allclose(m.as_field().sample_batch(pos), g[f"{tag}_field"], atol=1e-5, rtol=0)
+    # the same network as the true-miss decoder of both frame schedules
+    from paper_2504_18001_b200.harness import OrbitTrajectory
+    from paper_2504_18001_b200.session import RenderSession, SessionConfig
+
+    traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=48, height=48)
+    imgs = []
+    for march in ("parity", "throughput"):
+        cfg = SessionConfig(cached=False, loader="inline", policy=P.LodPolicy(1.2, 0), seed=0)
+        s = RenderSession(m.as_field(), P.grayscale_ramp(0.8), traj.camera_at(3), cfg, march=march)
+        img, rec = s.render_frame()
+        assert rec.true_misses == rec.samples > 0
+        imgs.append(img)
+    np.testing.assert_array_equal(imgs[0], imgs[1])  # uncached: no RNG, same values
+
+
 def test_brick_decode_into_pool_layout():
     """vcb_field_bricks writes [slot][z][y][x] exactly like pool.store (P15)."""
     from gpu_runner import product_inr
