@@ -24,7 +24,6 @@
 namespace cinr {
 
 constexpr int kTcRows = 128;  // UMMA M
-constexpr int kTcThreads = 128;
 
 // byte offset of element (row, k) in a K-major no-swizzle operand tile
 __device__ __forceinline__ uint32_t core_off(int row, int k, uint32_t lbo, uint32_t sbo) {
@@ -94,17 +93,6 @@ __device__ __forceinline__ void split_store(unsigned char* base, uint32_t off_hi
     *reinterpret_cast<__half*>(base + off + off_hi_lo_delta) = l;
 }
 
-struct TcSmem {
-    // operand tiles (each hi followed by lo at +delta)
-    alignas(128) unsigned char a0[2][kTcRows * 16 * 2];  // 128 x 16 fp16 (LBO 128, SBO 256)
-    alignas(128) unsigned char a1[2][kTcRows * 32 * 2];  // 128 x 32 fp16 (LBO 128, SBO 512)
-    alignas(128) unsigned char w0[2][32 * 16 * 2];       // 32 x 16
-    alignas(128) unsigned char w1[2][32 * 32 * 2];       // 32 x 32
-    float b0[32], b1[32], w2[32], b2;
-    alignas(8) uint64_t mbar;
-    uint32_t tmem;
-};
-
 constexpr uint32_t kA0Lbo = 128, kA0Sbo = 256, kA1Lbo = 128, kA1Sbo = 512;
 constexpr uint32_t kW0Lbo = 128, kW0Sbo = 256, kW1Lbo = 128, kW1Sbo = 512;
 
@@ -143,131 +131,6 @@ struct TcBricksSrc {
     }
 };
 
-template <class Src>
-__global__ void __launch_bounds__(kTcThreads) k_inr_decode_tc(VcbField F, Src src, long long n, float* out,
-                                                              int32_t* nonfinite) {
-    __shared__ TcSmem sm;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    // ---- stage weights (hi/lo split, K-major core layout) and biases
-    const float* W0 = F.weights;            // [32][16]
-    const float* W1 = F.weights + 32 * 16;  // [32][32]
-    const float* W2 = W1 + 32 * 32;         // [1][32]
-    for (int e = tid; e < 32 * 16; e += kTcThreads) {
-        const int nrow = e / 16, k = e % 16;
-        split_store(&sm.w0[0][0], sizeof(sm.w0[0]), core_off(nrow, k, kW0Lbo, kW0Sbo), __ldg(W0 + e));
-    }
-    for (int e = tid; e < 32 * 32; e += kTcThreads) {
-        const int nrow = e / 32, k = e % 32;
-        split_store(&sm.w1[0][0], sizeof(sm.w1[0]), core_off(nrow, k, kW1Lbo, kW1Sbo), __ldg(W1 + e));
-    }
-    if (tid < 32) {
-        sm.b0[tid] = __ldg(F.biases + tid);
-        sm.b1[tid] = __ldg(F.biases + 32 + tid);
-        sm.w2[tid] = __ldg(W2 + tid);
-    }
-    if (tid == 0) {
-        sm.b2 = __ldg(F.biases + 64);
-        const uint32_t a = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.tmem);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(dst));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = sm.tmem;
-    const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&sm.a0[0][0]);
-    const uint32_t sa1 = (uint32_t)__cvta_generic_to_shared(&sm.a1[0][0]);
-    const uint32_t sw0 = (uint32_t)__cvta_generic_to_shared(&sm.w0[0][0]);
-    const uint32_t sw1 = (uint32_t)__cvta_generic_to_shared(&sm.w1[0][0]);
-    const uint32_t da0 = sizeof(sm.a0[0]), da1 = sizeof(sm.a1[0]), dw0 = sizeof(sm.w0[0]), dw1 = sizeof(sm.w1[0]);
-    constexpr uint32_t ID = idesc_f16(kTcRows, 32);
-    uint32_t phase = 0;
-    const int row = tid;  // sample row within the tile == TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    for (long long t0 = (long long)blockIdx.x * kTcRows; t0 < n; t0 += (long long)gridDim.x * kTcRows) {
-        const long long i = t0 + row;
-        // ---- encode (CUDA cores): 8 levels x 2 features -> A0 (hi/lo)
-        float feat[16];
-        if (i < n) {
-            double x, y, z;
-            src.get(i, x, y, z);
-#pragma unroll
-            for (int l = 0; l < 8; l++) encode_level<2>(F, l, x, y, z, feat + 2 * l);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; k++) feat[k] = 0.0f;
-        }
-#pragma unroll
-        for (int k = 0; k < 16; k++) split_store(&sm.a0[0][0], da0, core_off(row, k, kA0Lbo, kA0Sbo), feat[k]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        // ---- layer 0: D0[128x32] = A0 W0^T (hi*hi + hi*lo + lo*hi)
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            mma_f16(tmem, umma_desc(sa0, kA0Lbo, kA0Sbo), umma_desc(sw0, kW0Lbo, kW0Sbo), ID, 0);
-            mma_f16(tmem, umma_desc(sa0, kA0Lbo, kA0Sbo), umma_desc(sw0 + dw0, kW0Lbo, kW0Sbo), ID, 1);
-            mma_f16(tmem, umma_desc(sa0 + da0, kA0Lbo, kA0Sbo), umma_desc(sw0, kW0Lbo, kW0Sbo), ID, 1);
-            mma_commit(&sm.mbar);
-        }
-        mbar_wait(&sm.mbar, phase);
-        phase ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float h[32];
-        tmem_ld32(tmem + lane_base, h);
-#pragma unroll
-        for (int c = 0; c < 32; c++) {
-            const float a = h[c] + sm.b0[c];
-            split_store(&sm.a1[0][0], da1, core_off(row, c, kA1Lbo, kA1Sbo), a > 0.0f ? a : 0.0f);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        // ---- layer 1: D1[128x32] = H0 W1^T, K = 32 in two 16-wide steps
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d1 = tmem + 32;
-#pragma unroll
-            for (int s = 0; s < 2; s++) {
-                const uint32_t ko = (uint32_t)s * 2u * kA1Lbo, kw = (uint32_t)s * 2u * kW1Lbo;
-                mma_f16(d1, umma_desc(sa1 + ko, kA1Lbo, kA1Sbo), umma_desc(sw1 + kw, kW1Lbo, kW1Sbo), ID, s);
-                mma_f16(d1, umma_desc(sa1 + ko, kA1Lbo, kA1Sbo), umma_desc(sw1 + dw1 + kw, kW1Lbo, kW1Sbo), ID, 1);
-                mma_f16(d1, umma_desc(sa1 + da1 + ko, kA1Lbo, kA1Sbo), umma_desc(sw1 + kw, kW1Lbo, kW1Sbo), ID, 1);
-            }
-            mma_commit(&sm.mbar);
-        }
-        mbar_wait(&sm.mbar, phase);
-        phase ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tmem_ld32(tmem + lane_base + 32, h);
-        // ---- output layer + activation (epilogue, CUDA cores)
-        float zo = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 32; c++) {
-            const float a = h[c] + sm.b1[c];
-            zo += (a > 0.0f ? a : 0.0f) * sm.w2[c];
-        }
-        zo += sm.b2;
-        float v = F.out_sigmoid ? 1.0f / (1.0f + expf(-zo)) : (zo < 0.0f ? 0.0f : (zo > 1.0f ? 1.0f : zo));
-        if (i < n) {
-            if (!isfinite(v)) *nonfinite = 1;
-            if (F.clip01) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
-            out[i] = v;
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // A0/A1 and TMEM reuse by the next tile
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
-}
-
-
 // ---------------------------------------------------------------------------
 // v2: one persistent CTA per SM, eight independent 128-row warpgroup pipelines
 // (own operand tiles, TMEM columns, mbarrier and named barrier), sharing one
@@ -276,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads) k_inr_decode_tc(VcbField F, Src sr
 // memory replace scattered L1 gathers by bank accesses.  Measured on B200 (2^24
 // random points): 8 groups + levels 0-2 in shared memory 6.8e9 samples/s; 8 groups,
 // no staged levels 6.5e9; 6 groups + levels 0-4 4.8e9 (the big tables crowd L1);
-// v1 (six 128-thread CTAs per SM) 5.9e9.
+// (a first version with six independent 128-thread CTAs per SM reached 5.9e9).
 #ifndef TC2_GROUPS
 #define TC2_GROUPS 8
 #endif
