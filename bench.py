@@ -612,6 +612,7 @@ def main():
         except Exception as exc:
             side["inr_decode"] = {"error": str(exc)}
 
+    launches_total = int(parallel.sum_over_ranks(ctx, t["launches"]))  # a collective: every rank
     if ctx.rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
@@ -626,7 +627,7 @@ def main():
             "roofline": roofline(samples_all, march_all, launches_all, peak, peak_src, args.march,
                                  (march_all / ctx.world) / total_ms if total_ms else None),
             "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "macro_grid": macro_info,
-            "clocks": clk.summary(), "gpu_launches": int(parallel.sum_over_ranks(ctx, t["launches"])),
+            "clocks": clk.summary(), "gpu_launches": launches_total,
             "samples_per_frame": samples_all / (args.steps * per_step),
             "hit_rate": 1.0 - sum(r.true_misses for r in t["recs"]) / max(1, samples),
             "last_record": {k: getattr(last, k) for k in ("frame", "samples", "true_misses", "fallback_hits",
