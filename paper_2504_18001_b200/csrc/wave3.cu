@@ -200,6 +200,7 @@ __device__ __forceinline__ void w3_retire(const VcbFrameParams& p, int pix, doub
 }
 
 struct W3Smem {
+    int4 lv[VCB_MAX_LOD];  // per LoD: brick grid + page-table offset (no indexed constant loads)
     int wsum[32];
     unsigned long long cnt[3];
 };
@@ -475,6 +476,9 @@ __global__ void __launch_bounds__(NT, 1)
     int* s_sc = reinterpret_cast<int*>(dsm + s.sm_sc);
     const float* lut = s_lut ? s_lut : p.lut;
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0;
+    if (threadIdx.x <= p.probe.max_lod && threadIdx.x < VCB_MAX_LOD)
+        sm.lv[threadIdx.x] = make_int4((int)p.probe.grid[threadIdx.x][0], (int)p.probe.grid[threadIdx.x][1],
+                                       (int)p.probe.grid[threadIdx.x][2], (int)p.probe.offset[threadIdx.x]);
     __syncthreads();
 
     unsigned c_ex = 0, c_fb = 0, c_ms = 0;  // per-thread sample counts (< 2^32)
@@ -664,21 +668,18 @@ __global__ void __launch_bounds__(NT, 1)
                         }
                         int rq, slot;
                         const int sv = probe_one(px, py, pz, dist, u, p.probe, p.table, p.pool,
-                                                 (long long*)p.last_used, p.cache_frame, v, rq, slot);
+                                                 (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv);
                         if (sv != rq) {
                             // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
                             const i64 span = p.probe.b << rq;
                             const double nx = clampd(DSUB(DMUL(px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
                             const double ny = clampd(DSUB(DMUL(py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
                             const double nz = clampd(DSUB(DMUL(pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
-                            const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][0] - 1);
-                            const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][1] - 1);
-                            const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0,
-                                                  p.probe.grid[rq][2] - 1);
-                            warp_aggregated_add(p.miss_count, p.probe.offset[rq] + bx +
-                                                                  p.probe.grid[rq][0] * (by + p.probe.grid[rq][1] * bz));
+                            const int4 q = sm.lv[rq];
+                            const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, q.x - 1);
+                            const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, q.y - 1);
+                            const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, q.z - 1);
+                            warp_aggregated_add(p.miss_count, (i64)q.w + bx + (i64)q.x * (by + (i64)q.y * bz));
                         }
                         if (sv < 0) {
                             queued = 1;
