@@ -208,6 +208,9 @@ typedef struct {
                                 the next frame; inserted at the next maintenance as InlineLoader /
                                 ThreadLoader collect() would); 0: decoded inside this call */
     int32_t pad2_;
+    int32_t *pending_list;   /* [total] bricks with a request-table entry (req_base >= 0), any order;
+                                kept by the maintenance (new keys appended, popped keys compacted out) */
+    int32_t *list_counts;    /* [1] pending_list entries; both null = k_pending scans every brick */
 } VcbMaintParams;
 
 /* Path tracing (render/pathtrace.py:112-146, session.py:108-109): samples_per_pixel

@@ -94,7 +94,8 @@ class VcbMaintParams(C.Structure):
                 ("table", vp), ("pool", vp), ("owner", vp), ("last_used", vp), ("miss_count", vp),
                 ("req_base", vp), ("req_hits", vp), ("state", vp), ("staging", vp), ("staged_keys", vp),
                 ("workspace", vp), ("workspace_bytes", i64), ("dbg_reports", vp), ("field", VcbField),
-                ("frame_stats", vp), ("decode_budget", i64), ("defer_decode", i32), ("pad2_", i32)]
+                ("frame_stats", vp), ("decode_budget", i64), ("defer_decode", i32), ("pad2_", i32),
+                ("pending_list", vp), ("list_counts", vp)]
 
 
 class VcbPtParams(C.Structure):

@@ -225,6 +225,10 @@ class DeviceCache:
         wsb = N.load().vcb_maint_workspace_bytes(lay.total, self.slots, mr)
         self.workspace = torch.zeros(wsb, dtype=torch.uint8, device=device)
         self.dbg_reports = t(2 * lay.total, torch.int64, 0) if debug else None
+        # the request table's keys as a compacted list (k_pending reads it instead of
+        # scanning every brick's req_base: 19.4 M bricks at 4096^3@B16); list_counts[1]
+        self.pending_list = t(lay.total, torch.int32, 0)
+        self.list_counts = t(4, torch.int32, 0)
         self.frame = 0  # Mrpd.frame: the probe stamp clock (P11)
         max_lin = max(counts) - 1
         self.lin_bits = _bits(max_lin)
@@ -241,6 +245,7 @@ class DeviceCache:
         self.miss_count.zero_()
         self.req_base.fill_(-1)
         self.req_hits.zero_()
+        self.list_counts.zero_()
         self.state.zero_()
 
     def maint_params(self, session_frame: int, field_desc, frame_stats=None, defer_decode=False) -> N.VcbMaintParams:
@@ -269,6 +274,7 @@ class DeviceCache:
         p.dbg_reports = ptr(self.dbg_reports)
         p.field = field_desc
         p.frame_stats = frame_stats
+        p.pending_list, p.list_counts = ptr(self.pending_list), ptr(self.list_counts)
         budget = getattr(self.sched, "decode_budget", None)
         p.decode_budget = -1 if budget is None else int(budget)
         p.defer_decode = 1 if defer_decode else 0

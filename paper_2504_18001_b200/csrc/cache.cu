@@ -72,23 +72,49 @@ __global__ void k_maint_gate(VcbMaintParams P, MaintWs w) {
     *w.n_dec() = 0;
 }
 
+// drain_miss_reports + report_many (mrpd.py:263, scheduler.py:60-72): a scan of the
+// per-brick counters, four at a time (the frame kernels' fire-and-forget reductions
+// stay cheap that way; 78 MB at 4096^3@B16); a key new to the request table joins the
+// pending list
+__device__ __forceinline__ void report_brick(const VcbMaintParams& P, long long b, int c) {
+    P.miss_count[b] = 0;
+    if (P.req_base[b] < 0) {
+        P.req_base[b] = P.session_frame;
+        P.req_hits[b] = c - 1;
+        if (P.list_counts != nullptr) P.pending_list[atomicAdd(P.list_counts + 1, 1)] = (int32_t)b;
+    } else {
+        P.req_hits[b] += c;
+    }
+}
+
 __global__ void k_report(VcbMaintParams P, MaintWs w) {
     if (maint_skipped(w)) return;
-    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
-         b += (long long)gridDim.x * blockDim.x) {
-        const int c = P.miss_count[b];
-        if (c == 0) continue;
-        P.miss_count[b] = 0;
-        if (P.req_base[b] < 0) {
-            P.req_base[b] = P.session_frame;
-            P.req_hits[b] = c - 1;
+    const long long n4 = P.total >> 2;
+    const int4* mc4 = reinterpret_cast<const int4*>(P.miss_count);  // cudaMalloc'd: 16-byte aligned
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        int c4[4];
+        if (i < n4) {
+            const int4 v = __ldcs(mc4 + i);
+            c4[0] = v.x;
+            c4[1] = v.y;
+            c4[2] = v.z;
+            c4[3] = v.w;
         } else {
-            P.req_hits[b] += c;
+#pragma unroll
+            for (int q = 0; q < 4; q++) c4[q] = (4 * i + q < P.total) ? P.miss_count[4 * i + q] : 0;
         }
-        const int r = atomicAdd(&w.ctr[1], 1);
-        if (P.dbg_reports) {
-            P.dbg_reports[2 * r] = b;
-            P.dbg_reports[2 * r + 1] = c;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int c = c4[q];
+            if (c == 0) continue;
+            const long long b = 4 * i + q;
+            report_brick(P, b, c);
+            const int r = atomicAdd(&w.ctr[1], 1);
+            if (P.dbg_reports) {
+                P.dbg_reports[2 * r] = b;
+                P.dbg_reports[2 * r + 1] = c;
+            }
         }
     }
 }
@@ -291,6 +317,18 @@ __device__ __forceinline__ unsigned long long composite_key(const VcbMaintParams
 
 __global__ void k_pending(VcbMaintParams P, MaintWs w) {
     if (maint_skipped(w)) return;
+    if (P.list_counts != nullptr) {
+        // the pending list holds exactly the keys with req_base >= 0
+        const long long n = P.list_counts[1];
+        if (blockIdx.x == 0 && threadIdx.x == 0) w.ctr[0] = (int)n;
+        for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n;
+             o += (long long)gridDim.x * blockDim.x) {
+            const long long b = P.pending_list[o];
+            w.pend_flat[o] = b;
+            w.pend_key[o] = (long long)composite_key(P, b) | (P.table[b] >= 0 ? (1ll << 63) : 0ll);
+        }
+        return;
+    }
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < P.total;
          b += (long long)gridDim.x * blockDim.x) {
         if (P.req_base[b] < 0) continue;
@@ -330,6 +368,18 @@ __global__ void __launch_bounds__(kSelThreads) k_select(VcbMaintParams P, MaintW
     for (long long i = threadIdx.x; i < np; i += blockDim.x) {
         const unsigned long long k = (unsigned long long)w.pend_key[i] & ~(1ull << 63);
         if (k <= thresh) P.req_base[w.pend_flat[i]] = -1;  // popped (returned or dropped)
+    }
+    if (P.list_counts != nullptr) {
+        // the surviving entries form the next pending list (w.pend_flat holds this one)
+        __shared__ int n_keep;
+        if (threadIdx.x == 0) n_keep = 0;
+        __syncthreads();
+        for (long long i = threadIdx.x; i < np; i += blockDim.x) {
+            const long long b = w.pend_flat[i];
+            if (P.req_base[b] >= 0) P.pending_list[atomicAdd(&n_keep, 1)] = (int32_t)b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) P.list_counts[1] = n_keep;
     }
     const unsigned long long lowmask = (1ull << (P.lin_bits + P.lod_bits)) - 1;
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -394,6 +444,8 @@ __global__ void k_post_decode(VcbMaintParams P, MaintWs w) {
         // InlineLoader.dispatch failure: keys re-enter with base = f, hits = 0
         for (long long i = 0; i < st->n_staged; i++) {
             const long long b = P.staged_keys[i];
+            if (P.list_counts != nullptr && P.req_base[b] < 0)
+                P.pending_list[P.list_counts[1]++] = (int32_t)b;
             P.req_base[b] = P.session_frame;
             P.req_hits[b] = 0;
         }
