@@ -207,18 +207,24 @@ class RenderSession:
         self.frame = 0
 
     # -- frame cycle (session.py:105-130)
-    def _frame_params(self, image):
-        cam = self.camera
+    def _static_key(self, W, H):
+        """Everything the frame parameters depend on besides the camera pose and the
+        per-frame clocks (settings are re-read each frame, as the reference does)."""
         cfg = self.config
         s = cfg.settings
-        W, H = int(cam.width), int(cam.height)
+        m, c = self.macro, self.cache
+        return (W, H, self.band, tuple(m.grid_dims), m.cell_size, ptr(self._lut), self._lut.shape[0], ptr(self._mu),
+                bytes(self._dfield.desc), ptr(c.table) if c is not None else 0, ptr(self._stats),
+                s.adaptive_step, s.skip_empty, s.base_step_scale, s.mu_floor, s.early_termination,
+                tuple(s.background), s.max_iterations, cfg.policy.mode, getattr(cfg.scheduler, "decode_budget", None))
+
+    def _frame_template(self, W, H):
+        """The frame parameters that stay fixed between frames, as raw bytes (host
+        submission is on the frame's critical path: the GPU waits for the first launch)."""
+        cfg = self.config
+        s = cfg.settings
         p = N.VcbFrameParams()
-        rot, tan_h, tan_v = camera_rays_setup(cam)
-        for a in range(3):
-            p.cam.origin[a] = float(cam.position[a])
-        for i in range(9):
-            p.cam.rot[i] = float(rot.ravel()[i])
-        p.cam.tan_h, p.cam.tan_v, p.cam.width, p.cam.height = tan_h, tan_v, W, H
+        p.cam.width, p.cam.height = W, H
         row0, step = self.band
         p.cam.row0, p.cam.row_step, p.cam.rows = row0, step, self._band_rows(H)
         vx, vy, vz = self.dims
@@ -234,11 +240,8 @@ class RenderSession:
             raise ValueError(f"unknown stochastic lod mode {pol.mode!r}")
         c = self.cache
         if c is not None:
-            force = force_max_scale(c.max_lod, point_to_unit_box(np.asarray(cam.position, dtype=np.float64)))
-            scale = effective_lod_scale(pol, self.frame, force)
             lay = c.layout
             p.probe.vx, p.probe.vy, p.probe.vz = float(vx), float(vy), float(vz)
-            p.probe.lod_scale = scale
             p.probe.mode = MODES[pol.mode]
             p.probe.max_lod = c.max_lod
             p.probe.b = lay.brick_size
@@ -249,27 +252,47 @@ class RenderSession:
                 p.probe.offset[l] = lay.offsets[l]
             p.cached = 1
             p.paged_dist = 1 if c.paged else 0
-            p.cache_frame = c.frame
             p.table, p.pool, p.last_used, p.miss_count = ptr(c.table), ptr(c.pool), ptr(c.last_used), ptr(c.miss_count)
-        p.rng_base = frame_rng_base(cfg.seed, self.frame)
         p.term = float(s.early_termination)
         for a in range(3):
             p.bg[a] = float(s.background[a])
         p.lut_size = self._lut.shape[0]
         p.max_iterations = int(s.max_iterations)
-        p.epoch = _next_epoch()
-        p.timing = (1 if self.timing else 0) | (2 if self.trace else 0)
-        p.impl = self.impl
         p.mu, p.lut = ptr(self._mu), ptr(self._lut)
         p.field = self._dfield.desc
-        p.image = ptr(image)
-        p.image_global = 1 if (self._target is not None and image is self._target) else 0
         budget = getattr(cfg.scheduler, "decode_budget", None)
         p.miss_budget = -1 if budget is None else int(budget)
         p.stats = ptr(self._stats)
-        need = N.load().vcb_frame_workspace_bytes(W * p.cam.rows, p.max_iterations)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        self._ws_need = N.load().vcb_frame_workspace_bytes(W * p.cam.rows, p.max_iterations)
+        return bytes(p)
+
+    def _frame_params(self, image):
+        cam = self.camera
+        cfg = self.config
+        W, H = int(cam.width), int(cam.height)
+        key = self._static_key(W, H)
+        if getattr(self, "_tmpl_key", None) != key:
+            self._tmpl = self._frame_template(W, H)
+            self._tmpl_key = key
+        p = N.VcbFrameParams.from_buffer_copy(self._tmpl)
+        # per frame: the camera pose, the LoD scale of the preload ramp, the clocks
+        rot, tan_h, tan_v = camera_rays_setup(cam)
+        p.cam.origin[:] = [float(x) for x in cam.position]
+        p.cam.rot[:] = [float(x) for x in rot.ravel()]
+        p.cam.tan_h, p.cam.tan_v = tan_h, tan_v
+        c = self.cache
+        if c is not None:
+            force = force_max_scale(c.max_lod, point_to_unit_box(np.asarray(cam.position, dtype=np.float64)))
+            p.probe.lod_scale = effective_lod_scale(cfg.policy, self.frame, force)
+            p.cache_frame = c.frame
+        p.rng_base = frame_rng_base(cfg.seed, self.frame)
+        p.epoch = _next_epoch()
+        p.timing = (1 if self.timing else 0) | (2 if self.trace else 0)
+        p.impl = self.impl
+        p.image = ptr(image)
+        p.image_global = 1 if (self._target is not None and image is self._target) else 0
+        if self._ws is None or self._ws.numel() < self._ws_need:
+            self._ws = torch.empty(self._ws_need, dtype=torch.uint8, device=self.device)
         p.workspace = ptr(self._ws)
         p.workspace_bytes = self._ws.numel()
         return p
