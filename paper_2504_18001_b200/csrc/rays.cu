@@ -45,20 +45,51 @@ struct RmCfg {
     int max_it;
     int max_skip;                        // empty macro cells one lane crosses per loop turn (0 = all)
     long long n_tickets;                 // 32 per 8x4 tile
+    uint32_t* coarse;                    // [words] non-empty 4x4x4 super-cells (kFast 2), in the workspace
+    int coarse_words;
     double4* ray_a;                      // [n] dx, dy, dz, t_enter of the box-hitting rays
     double2* ray_b;                      // [n] t_exit, (local pixel, film pixel) as two int32
     int* n_rays;                         // rays in the list (written by k_ray_setup)
 };
 
 // workspace after frame_ws_layout(0, ...): the ray list
+constexpr int kCoarseMaxWords = 48 * 1024 / 4;  // super-cell bits kept in shared memory (48 KB)
+
 inline int64_t rays_layout(int64_t npix, void* base, RmCfg* c) {
     const size_t a = align_up((size_t)npix * sizeof(double4), 256);
     const size_t b = align_up((size_t)npix * sizeof(double2), 256);
+    const size_t o = align_up((size_t)kCoarseMaxWords * 4, 256);
     if (base && c) {
         c->ray_a = reinterpret_cast<double4*>(base);
         c->ray_b = reinterpret_cast<double2*>((char*)base + a);
+        c->coarse = reinterpret_cast<uint32_t*>((char*)base + a + b);
     }
-    return (int64_t)(a + b);
+    return (int64_t)(a + b + o);
+}
+
+// Bitmask of the 4x4x4 super-cells of the macro grid holding any cell with a positive
+// majorant (one warp per 32 super-cells; recomputed each frame, ~67 MB read at 4096^3).
+__global__ void k_coarse_occ(const float* __restrict__ mu, int gx, int gy, int gz, uint32_t* out, int words) {
+    const int lane = threadIdx.x & 31;
+    const int sgx = (gx + 3) >> 2, sgy = (gy + 3) >> 2, sgz = (gz + 3) >> 2;
+    const long long nsc = (long long)sgx * sgy * sgz;
+    for (long long wd = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; wd < words;
+         wd += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long sc = wd * 32 + lane;
+        bool any = false;
+        if (sc < nsc) {
+            const int sx = (int)(sc % sgx), sy = (int)((sc / sgx) % sgy), sz = (int)(sc / ((long long)sgx * sgy));
+            for (int z = sz * 4; z < min(sz * 4 + 4, gz) && !any; z++)
+                for (int y = sy * 4; y < min(sy * 4 + 4, gy) && !any; y++)
+                    for (int x = sx * 4; x < min(sx * 4 + 4, gx); x++)
+                        if (__ldg(mu + x + (long long)gx * (y + (long long)gy * z)) > 0.0f) {
+                            any = true;
+                            break;
+                        }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, any);
+        if (lane == 0) out[wd] = b;
+    }
 }
 
 int64_t rays_ws_bytes(int64_t npix, int max_it) {
@@ -156,6 +187,10 @@ __global__ void __launch_bounds__(NT, 1)
         float* m = reinterpret_cast<float*>(dsm + cfg.sm_mu);
         for (long long i = threadIdx.x; i < cells; i += NT) m[i] = __ldg(p.mu + i);
         mu_s = m;
+    } else if (kFast == 2) {
+        uint32_t* o = reinterpret_cast<uint32_t*>(dsm + cfg.sm_occ);
+        for (int i = threadIdx.x; i < cfg.coarse_words; i += NT) o[i] = __ldcg(cfg.coarse + i);
+        occ = o;
     } else if (cfg.sm_occ >= 0) {
         uint32_t* o = reinterpret_cast<uint32_t*>(dsm + cfg.sm_occ);
         const int nwords = (int)((cells + 31) >> 5);
@@ -246,9 +281,9 @@ __global__ void __launch_bounds__(NT, 1)
             if (k < cfg.max_it) {
                 double cf = __longlong_as_double(cur);
                 i64 ck = cur;
-                if constexpr (kFast)
-                    f = advance_impl<1>(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
-                                        cfg.max_skip);
+                if constexpr (kFast != 0)
+                    f = advance_impl<kFast>(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s,
+                                            nullptr, cfg.max_skip);
                 else
                     f = advance_one(ox, oy, oz, dx, dy, dz, ten, tex, cf, ck, p.adv, p.mu, a, occ, mu_s, nullptr,
                                     cfg.max_skip);
@@ -396,7 +431,10 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
-static const void* ray_kernel(int mode, int nt, bool fast) {
+static const void* ray_kernel(int mode, int nt, int fast) {
+    if (fast == 2)
+        return mode == 1 ? (const void*)k_ray_march<1, 512, 2>
+                         : mode == 2 ? (const void*)k_ray_march<2, 512, 2> : (const void*)k_ray_march<0, 512, 2>;
     if (fast) {
         if (nt == 640)
             return mode == 1 ? (const void*)k_ray_march<1, 640, 1>
@@ -449,8 +487,22 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     if (off + 16 + cells * 4 <= kSmemMax) cfg.sm_mu = take((int)cells * 4);
     else if (p.adv.skip_empty && off + 16 + ((cells + 31) >> 5) * 4 <= kSmemMax)
         cfg.sm_occ = take((int)(((cells + 31) >> 5) * 4));
-    const bool fast = cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty;
+    int fast = (cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty) ? 1 : 0;
+    cfg.coarse_words = 0;
+    if (!fast && cfg.sm_occ < 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty && cells > 0) {
+        // majorants too large for shared memory (4096^3: 256^3 cells): super-cell bits
+        const long long nsc = (long long)((p.adv.gx + 3) / 4) * ((p.adv.gy + 3) / 4) * ((p.adv.gz + 3) / 4);
+        const int words = (int)((nsc + 31) / 32);
+        if (words <= kCoarseMaxWords) {
+            // (the plain occupancy bitmask chosen above is dropped in this mode)
+            cfg.sm_occ = take(words * 4);
+            cfg.coarse_words = words;
+            fast = 2;
+        }
+    }
     if (mode == 2 || !fast) nt = 512;
+    if (fast == 2) nt = 512;
+    if (off > kSmemMax) return set_error("march_frame: %d B of shared memory needed", off);
     const void* fn = ray_kernel(mode, nt, fast);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
     int per_sm = 0;
@@ -459,6 +511,9 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     const int G = device_sms();
     if (ev) cudaEventRecord(ev[0], st);
+    if (fast == 2)
+        k_coarse_occ<<<grid_for((int64_t)cfg.coarse_words * 32, 256), 256, 0, st>>>(
+            p.mu, (int)p.adv.gx, (int)p.adv.gy, (int)p.adv.gz, cfg.coarse, cfg.coarse_words);
     k_ray_setup<<<grid_for(cfg.n_tickets, 256), 256, 0, st>>>(p, cfg);
     VcbFrameParams pc = p;
     FrameCounters* ctr = w.ctr;
@@ -469,7 +524,7 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
         *ev_used = 1;
     }
     if (e != cudaSuccess) return set_error("march_frame: ray kernel launch: %s", cudaGetErrorString(e));
-    *launches = 2;
+    *launches = fast == 2 ? 3 : 2;
     return check_launch("march_frame(rays)");
 }
 
