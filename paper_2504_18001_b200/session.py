@@ -116,6 +116,8 @@ class RenderSession:
         # maintenance selects is decoded on a decode stream while the next frame marches, and
         # inserted by the next maintenance (the inline cadence, P12, so state is identical)
         self._dstream = torch.cuda.Stream(self.device) if (config.loader == "thread" and config.cached) else None
+        self._cstream = torch.cuda.Stream(self.device)  # device-to-host image copies
+        self._ev_image = torch.cuda.Event()
         self._ev_decoded = None
 
     MARCH_SCHEDULES = {"parity": 0, "throughput": 10}
@@ -385,6 +387,8 @@ class RenderSession:
                 N.call("vcb_pathtrace_frame", C.byref(p), C.byref(q), stream_ptr(self.stream))
             else:
                 N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
+            # the image is final here: a host copy can overlap the maintenance below
+            self._ev_image.record(self.stream)
             if self.cache is not None:
                 # a frame whose true-miss inference failed raises RenderError in collect_record
                 # without advancing the clocks; its maintenance skips itself on the device
@@ -434,9 +438,13 @@ class RenderSession:
         t0 = time.perf_counter()
         img = self.render_frame_device()
         host = self._pinned(tuple(img.shape))
-        with torch.cuda.stream(self.stream):
+        # the copy waits only for the frame kernel, not for the maintenance after it
+        self._cstream.wait_event(self._ev_image)
+        with torch.cuda.stream(self._cstream):
             host.copy_(img, non_blocking=True)
+            img.record_stream(self._cstream)
         rec = self.collect_record(t0)
+        self._cstream.synchronize()
         out = host.numpy()
         # the caller owns the array; its pinned buffer returns to the pool when it dies
         weakref.finalize(out, self._pin_free.append, host)
