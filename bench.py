@@ -371,6 +371,10 @@ def main():
     ap.add_argument("--no-other", action="store_true", help="skip the other march schedule")
     ap.add_argument("--config3-steps", type=int, default=10, help="config 3 (4096^3 virtual) timed frames (0 = skip)")
     ap.add_argument("--config3-preroll", type=int, default=60)
+    ap.add_argument("--config5-steps", type=int, default=5, help="config 5 at N=1 (4096^3, 4K) frames (0 = skip)")
+    ap.add_argument("--config5-preroll", type=int, default=20)
+    ap.add_argument("--config1", type=int, default=1, help="config 1 (64^3, 256^2, 120-frame orbit) side result")
+    ap.add_argument("--config4-frames", type=int, default=40, help="config 4 (2048^3, 1080p) frames (0 = skip)")
     ap.add_argument("--uncached-steps", type=int, default=5, help="frames of the no-cache INR baseline (0 = skip)")
     ap.add_argument("--scheduler-frames", type=int, default=8, help="frame-scheduler cold-start frames (0 = skip)")
     ap.add_argument("--budget", type=int, default=1 << 20, help="decode budget (samples/frame) of that comparison")
@@ -550,6 +554,12 @@ def main():
                 traceback.print_exc()
                 side["config3"] = {"error": str(exc)}
             torch.cuda.empty_cache()
+        # ---- configs 1 and 4 at their stated sizes
+        if args.config1:
+            side["config1"] = run_config1(P, SessionConfig, OrbitTrajectory, args, flush, dev)
+        if args.config4_frames > 0:
+            side["config4"] = run_config4(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev)
+            torch.cuda.empty_cache()
         # ---- the paper's comparison: no brick cache (every sample through the INR)
         if args.uncached_steps > 0:
             ucfg = session_config(P, SessionConfig, cached=False)
@@ -706,6 +716,93 @@ def run_config3(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev, 
         del s
         torch.cuda.empty_cache()
     out["target_60fps_met"] = out["throughput"]["fps"] >= 60.0
+    # BASELINE config 5 at N=1: the same 4096^3 volume at 3840x2160 (the per-GPU tile of
+    # the sort-first runs is a 1/N row band of this frame)
+    if args.config5_steps > 0:
+        t5 = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=3840, height=2160)
+        s = RenderSession(fld, P.warm_body(0.5, 0.9), t5.camera_at(0), cfg, macro=mg, device=dev, march="throughput")
+        preroll(s, t5.camera_at, args.config5_preroll)
+        f0 = args.config5_preroll
+        o = device_frames(s, t5.camera_at, range(f0, f0 + args.config5_steps), flush, s.stream, timing=True)
+        smp = sum(r.samples for r in o["recs"])
+        out["config5_n1"] = {"image": "3840x2160", "march": "throughput", "preroll": f0,
+                             "fps": len(o["ms"]) / (sum(o["ms"]) / 1000.0), "ms_per_frame": statistics.mean(o["ms"]),
+                             "samples_per_frame": smp / len(o["ms"]),
+                             "roofline": roofline(smp, o["march_ms"], o["march_launches"], peak, peak_src,
+                                                  "throughput", o["march_ms"] / sum(o["ms"]))}
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_config1(P, SessionConfig, OrbitTrajectory, args, flush, dev):
+    """BASELINE config 1 at its stated size: 64^3 random-init INR, B=16, the 2-level
+    paged MRPD knobs (direct_table_threshold=8, page_size=4, page_budget=2), 4^3 pool,
+    256x256, the 120-frame orbit; fps over the orbit's last 20 frames (harness.py:65-109's
+    summary window), device-timed and through render_frame()."""
+    from paper_2504_18001_b200 import macrocell
+    from paper_2504_18001_b200.session import RenderSession
+
+    dims = (64,) * 3
+    fld = make_model(64).as_field()
+    mg = macrocell.build(fld, dims, 16, dev)
+    cfg = SessionConfig(cached=True, loader="inline",
+                        cache=P.CacheConfig(brick_size=16, pool_dims=(4, 4, 4), direct_table_threshold=8, page_size=4,
+                                            page_budget=2),
+                        scheduler=P.SchedulerConfig(max_requests=40), policy=P.LodPolicy(1.2, 20),
+                        settings=P.RenderSettings(), seed=0)
+    traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=256, height=256)
+    out = {"volume": "64^3 random-init INR", "image": "256x256", "orbit_frames": 120, "window": "frames 100-119"}
+    for march in ("throughput", "parity"):
+        s = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, device=dev, march=march)
+        preroll(s, traj.camera_at, 100)
+        o = device_frames(s, traj.camera_at, range(100, 120), flush, s.stream)
+        s2 = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, device=dev, march=march)
+        s2.reserve_host_frames(2)
+        walls = []
+        for f in range(120):
+            s2.set_camera(traj.camera_at(f))
+            t0 = time.perf_counter()
+            s2.render_frame()
+            if f >= 100:
+                walls.append(time.perf_counter() - t0)
+        out[march] = {"fps": len(o["ms"]) / (sum(o["ms"]) / 1000.0), "e2e_fps": len(walls) / sum(walls),
+                      "hit_rate": 1.0 - sum(r.true_misses for r in o["recs"]) / max(1, sum(r.samples for r in o["recs"]))}
+        del s, s2
+    return out
+
+
+def run_config4(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev):
+    """BASELINE config 4: 2048^3 random-init INR, 1920x1080, saliency-ranked vs FIFO
+    scheduling (SchedulerConfig.ranking_enabled) along the orbit with a transfer-function
+    switch at frame 16: frames to a 90% hit rate (harness.py:78-86) and fps."""
+    from paper_2504_18001_b200.session import RenderSession
+
+    dims = (2048,) * 3
+    fld = make_model(2048).as_field()
+    mg = macrocell.build(fld, dims, 16, dev)
+    traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=1920, height=1080)
+    out = {"volume": "2048^3 random-init INR", "image": "1920x1080", "frames": args.config4_frames,
+           "event": "warm_body(0.5,0.9) -> warm_body(0.4,0.85) at frame 16"}
+    for label, ranked in (("ranked", True), ("fifo", False)):
+        cfg = SessionConfig(cached=True, loader="inline", cache=P.CacheConfig(brick_size=16, pool_dims=(48, 48, 48)),
+                            scheduler=P.SchedulerConfig(max_requests=40, ranking_enabled=ranked),
+                            policy=P.LodPolicy(1.2, 20), settings=P.RenderSettings(), seed=0)
+        s = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, device=dev,
+                          march="throughput")
+        recs, ms = [], []
+        for f in range(args.config4_frames):
+            if f == 16:
+                s.set_transfer_function(P.warm_body(0.4, 0.85))
+            o = device_frames(s, traj.camera_at, [f], flush, s.stream)
+            recs.append(o["recs"][0])
+            ms.append(o["ms"][0])
+        rates = [(r.samples - r.true_misses) / r.samples if r.samples else 0.0 for r in recs]
+        exact = [r.exact_hits / r.samples if r.samples else 0.0 for r in recs]
+        to90 = next((i for i, x in enumerate(rates) if x >= 0.9), -1)
+        out[label] = {"frames_to_hit_rate_0.9": to90, "fps_last_10": 10 / (sum(ms[-10:]) / 1000.0),
+                      "exact_lod_hit_rate_mean": float(np.mean(exact)), "exact_lod_hit_rate_last": exact[-1]}
+        del s
     return out
 
 

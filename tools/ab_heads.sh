@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # Same-box A/B of the working tree against .ab_head (a worktree of an earlier commit).
 set -u
-A="--no-ramp --no-other --scheduler-frames 0 --pt-steps 0 --train-steps 0 --decode-n 0 --uncached-steps 0 --no-cpu-baseline --no-e2e ${BENCH_ARGS:-}"
+A="--no-ramp --no-other --scheduler-frames 0 --pt-steps 0 --train-steps 0 --decode-n 0 --uncached-steps 0 --no-cpu-baseline --no-e2e --config1 0 --config4-frames 0 --config5-steps 0 ${BENCH_ARGS:-}"
 for rep in 1 2; do
   for t in . .ab_head; do
     (cd $t && timeout 300 python bench.py $A > /tmp/ab.json 2>/tmp/ab.err; python -c "

@@ -10,7 +10,7 @@ timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_ful
 if [ -z "${SKIP_REF:-}" ]; then
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc $? at $(( $(date +%s) - S ))s"
 fi
-Q="--no-cpu-baseline --no-e2e --no-ramp --no-other --decode-n 0 --pt-steps 0 --uncached-steps 0 --train-steps 0 --scheduler-frames 0 --config3-steps 0"
+Q="--no-cpu-baseline --no-e2e --no-ramp --no-other --decode-n 0 --pt-steps 0 --uncached-steps 0 --train-steps 0 --scheduler-frames 0 --config3-steps 0 --config1 0 --config4-frames 0"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 3 --warmup 3 --preroll 20 $Q > gpurun_out/ncu_list.out 2>&1; echo "list rc $?"
 # full captures: k_ray_march launch 63 (after a 60-frame pre-roll + 3 warm-up frames)
