@@ -36,6 +36,44 @@ int device_sms() {
     return sms;
 }
 
+// Resident CTAs per SM of `fn` at (threads, dynamic smem), after making sure its
+// dynamic shared-memory limit admits `smem` (the limit only ever grows: lowering it
+// for a small launch would break a later larger one).  The driver calls run once per
+// (device, kernel, size), not per frame.
+int kernel_ctas_per_sm(const void* fn, int threads, int smem) {
+    struct Limit {
+        const void* fn;
+        int dev, smem_max;
+    };
+    struct Occ {
+        const void* fn;
+        int dev, threads, smem, per_sm;
+    };
+    static thread_local Limit lim[32];
+    static thread_local Occ occ[64];
+    static thread_local int nl = 0, no = 0;
+    int d = 0;
+    cudaGetDevice(&d);
+    int li = -1;
+    for (int i = 0; i < nl; i++)
+        if (lim[i].fn == fn && lim[i].dev == d) li = i;
+    if (li < 0) {
+        li = nl < 32 ? nl++ : 0;
+        lim[li] = Limit{fn, d, 0};
+    }
+    if (smem > lim[li].smem_max) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        lim[li].smem_max = smem;
+    }
+    for (int i = 0; i < no; i++)
+        if (occ[i].fn == fn && occ[i].dev == d && occ[i].threads == threads && occ[i].smem == smem)
+            return occ[i].per_sm;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    occ[no < 64 ? no++ : 0] = Occ{fn, d, threads, smem, per_sm};
+    return per_sm;
+}
+
 }  // namespace cinr
 
 extern "C" const char* vcb_last_error(void) { return cinr::g_err; }

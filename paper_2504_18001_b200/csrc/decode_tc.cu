@@ -346,7 +346,7 @@ static int launch_tc2(const VcbField& F, const Src& src, long long n, float* out
                       cudaStream_t st, const int64_t* n_keys_dev = nullptr, long long per_key = 0) {
     const int L = tc2_smem_levels(F);
     const size_t smem = ((sizeof(Tc2Smem) + 127) & ~size_t(127)) + (size_t)(L > 0 ? F.tab_off[L] : 0) * 8;
-    cudaFuncSetAttribute(k_inr_decode_tc2<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_ctas_per_sm((const void*)k_inr_decode_tc2<Src>, kTc2Threads, (int)smem);  // raises the smem limit once
     const long long tiles = (n + kTcRows - 1) / kTcRows;
     long long grid = (tiles + kTc2Groups - 1) / kTc2Groups;
     if (grid > device_sms()) grid = device_sms();

@@ -504,9 +504,7 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     if (fast == 2) nt = 512;
     if (off > kSmemMax) return set_error("march_frame: %d B of shared memory needed", off);
     const void* fn = ray_kernel(mode, nt, fast);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, off);
+    const int per_sm = kernel_ctas_per_sm(fn, nt, off);
     if (per_sm < 1) return set_error("march_frame: ray kernel does not fit one CTA per SM (%d B shared)", off);
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     const int G = device_sms();

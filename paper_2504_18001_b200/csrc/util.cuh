@@ -10,6 +10,7 @@ namespace cinr {
 int set_error(const char* fmt, ...);
 int check_launch(const char* what);
 int device_sms();
+int kernel_ctas_per_sm(const void* fn, int threads, int smem);
 
 inline int grid_for(int64_t n, int block, int cap_per_sm = 16) {
     int64_t g = (n + block - 1) / block;

@@ -826,9 +826,7 @@ int launch_wave3_frame(const VcbFrameParams& p, cudaStream_t st, long long* laun
         s.sm_occ = take((int)(((cells + 31) >> 5) * 4));
     s.sm_total = off;
     const void* fn = wave3_kernel(mode, nt);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, off);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, off);
+    const int per_sm = kernel_ctas_per_sm(fn, nt, off);
     if (per_sm < 1)
         return set_error("march_frame: frame kernel does not fit one CTA per SM (%d B shared)", off);
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);

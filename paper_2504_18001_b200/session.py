@@ -376,7 +376,8 @@ class RenderSession:
                 self._img = torch.empty((R, W, 4), dtype=torch.float32, device=self.device)
             img = self._img
         with torch.cuda.stream(self.stream):
-            self._stats.zero_()
+            if self.mode == "pathtrace":
+                self._stats.zero_()  # (vcb_march_frame clears its counters itself)
             p = self._frame_params(img)
             if self.mode == "pathtrace":
                 if self.band != (0, 1):
