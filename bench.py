@@ -277,10 +277,14 @@ def preroll(sess, cam, n, start=0):
         sess.collect_record(t0)
 
 
-def roofline(samples, march_ms, launches, peak, peak_src, march, share=None):
+def roofline(samples, march_ms, launches, peak, peak_src, march, share=None, profile=None):
+    """`profile`: the ncu capture whose DRAM bytes are this kernel's `traffic`
+    (profiles/ncu_frame_kernel_<profile>.json; default <march>, the config-2 captures;
+    None-valued for workloads without a capture)."""
     achieved = samples * BYTES_PER_SAMPLE / (march_ms / 1000.0) / 1e9 if march_ms > 0 else None
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak if achieved else None, "traffic": profiled_traffic(march),
+            "frac": achieved / peak if achieved else None,
+            "traffic": profiled_traffic(profile if profile is not None else march),
             "kernel": KERNEL.get(march, march),
             "algorithmic_bytes": f"{BYTES_PER_SAMPLE} B/sample x {samples / max(launches, 1):.0f} samples per launch",
             "launches": launches, "avg_launch_us": 1000.0 * march_ms / max(launches, 1), "march_share_of_step": share,
@@ -712,7 +716,7 @@ def run_config3(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev, 
                       "true_misses_per_frame": sum(r.true_misses for r in o["recs"]) / len(o["ms"]),
                       "occupancy": lr.occupancy,
                       "roofline": roofline(smp, o["march_ms"], o["march_launches"], peak, peak_src, march,
-                                           o["march_ms"] / sum(o["ms"]))}
+                                           o["march_ms"] / sum(o["ms"]), profile=f"{march}_config3")}
         del s
         torch.cuda.empty_cache()
     out["target_60fps_met"] = out["throughput"]["fps"] >= 60.0
@@ -729,7 +733,7 @@ def run_config3(P, SessionConfig, OrbitTrajectory, macrocell, args, flush, dev, 
                              "fps": len(o["ms"]) / (sum(o["ms"]) / 1000.0), "ms_per_frame": statistics.mean(o["ms"]),
                              "samples_per_frame": smp / len(o["ms"]),
                              "roofline": roofline(smp, o["march_ms"], o["march_launches"], peak, peak_src,
-                                                  "throughput", o["march_ms"] / sum(o["ms"]))}
+                                                  "throughput", o["march_ms"] / sum(o["ms"]), profile="throughput_config5")}
         del s
         torch.cuda.empty_cache()
     return out

@@ -18,6 +18,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ra
     -o gpurun_out/prof_rays_c2 -f python bench.py --steps 1 --warmup 3 --preroll 60 $Q > gpurun_out/ncu_rays_c2.out 2>&1; echo "rays c2 rc $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wave3_march -s 62 -c 1 \
     -o gpurun_out/prof_wave3_c2 -f python bench.py --march parity --steps 1 --warmup 3 --preroll 60 $Q > gpurun_out/ncu_wave3_c2.out 2>&1; echo "wave3 c2 rc $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ray_march -s 60 -c 1 \
+    -o gpurun_out/prof_rays_c3 -f python tools/config3_probe.py 62 > gpurun_out/ncu_rays_c3.out 2>&1; echo "rays c3 rc $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_inr_decode_tc2 -s 2 -c 1 \
     -o gpurun_out/prof_decode_tc2 -f python tools/decode_bench.py > gpurun_out/ncu_decode.out 2>&1; echo "decode rc $?"
 echo "total $(( $(date +%s) - S ))s"
