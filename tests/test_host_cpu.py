@@ -151,3 +151,26 @@ def test_product_does_not_import_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_camera_basis_is_numpys_arithmetic():
+    """The scalar camera basis (render.camera_basis, host submission path) equals the
+    reference's numpy expressions (camera.py:36-42) bit for bit on random cameras."""
+    from paper_2504_18001_b200 import render as R
+
+    def numpy_basis(p, t, u):
+        fwd = np.asarray(t, dtype=np.float64) - np.asarray(p, dtype=np.float64)
+        fwd /= np.linalg.norm(fwd)
+        right = np.cross(fwd, np.asarray(u, dtype=np.float64))
+        right /= np.linalg.norm(right)
+        return fwd, right, np.cross(right, fwd)
+
+    class Cam:
+        pass
+
+    rng = np.random.default_rng(11)
+    for _ in range(20000):
+        c = Cam()
+        c.position, c.target, c.up = tuple(rng.uniform(-3, 3, 3)), tuple(rng.uniform(-1, 2, 3)), tuple(rng.normal(size=3))
+        for a, b in zip(numpy_basis(c.position, c.target, c.up), R.camera_basis(c)):
+            np.testing.assert_array_equal(a, b)
