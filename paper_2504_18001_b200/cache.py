@@ -21,48 +21,44 @@ from . import _native as N
 from .device import ptr, stream_ptr
 
 
-# ----------------------------------------------------------------- brick math
-def lod_stride(lod: int) -> int:
-    return 1 << lod
+# ----------------------------------------------------------------- brick hierarchy
+# The semantics are brickmath.py:25-151's (pinned by tests/golden/brickmath.npz): at
+# LoD L a brick holds B samples 2^L voxels apart; along an axis brick k starts at
+# native voxel k*B*2^L - 1 (0 for k = 0: P1) and owns the positions p with
+# floor((p + 1) / (B*2^L)) = k; an axis needs one brick at L once
+# V <= (B-1)*2^L + 1, else ceil((V + 2^L) / (B*2^L)).  Here every per-level quantity
+# is a row of a small table built once.
+
+_LOD_LIMIT = 48
 
 
-def brick_span(brick_size: int, lod: int) -> int:
-    return brick_size << lod
+def _axis_bricks(v: int, b: int, lod: int) -> int:
+    step = 1 << lod
+    return 1 if v <= (b - 1) * step + 1 else -(-(v + step) // (b << lod))
 
 
-def brick_origin(index, brick_size: int, lod: int):
-    """k*B*2^L - 1 for k > 0, 0 for k = 0 (brickmath.py:35-39; P1)."""
-    index = np.asarray(index, dtype=np.int64)
-    o = index * brick_span(brick_size, lod)
-    return np.where(index > 0, o - 1, o)
-
-
-def locate_axis(position, brick_size: int, lod: int):
-    return np.floor((np.asarray(position, dtype=np.float64) + 1.0) / brick_span(brick_size, lod)).astype(np.int64)
-
-
-def grid_dims_axis(voxels: int, brick_size: int, lod: int) -> int:
-    s = lod_stride(lod)
-    if voxels <= (brick_size - 1) * s + 1:
-        return 1
-    return int(-(-(voxels + s) // brick_span(brick_size, lod)))
-
-
-def grid_dims(dims, brick_size: int, lod: int):
-    return tuple(grid_dims_axis(v, brick_size, lod) for v in dims)
+def _level_table(dims, b: int):
+    """(L+1, 3) brick counts per level until one brick covers the volume."""
+    rows = []
+    while True:
+        lod = len(rows)
+        row = tuple(_axis_bricks(v, b, lod) for v in dims)
+        rows.append(row)
+        if row == (1, 1, 1):
+            return rows
+        if lod >= _LOD_LIMIT:
+            raise ValueError(f"dims {tuple(dims)} need more than {_LOD_LIMIT} LoD levels at brick size {b}")
 
 
 def max_lod(dims, brick_size: int) -> int:
-    lod = 0
-    while grid_dims(dims, brick_size, lod) != (1, 1, 1):
-        lod += 1
-        if lod > 48:
-            raise ValueError(f"no single-brick LoD for dims {dims} at brick size {brick_size}")
-    return lod
+    """The coarsest LoD (a single brick), brickmath.py:60-67."""
+    return len(_level_table(tuple(int(d) for d in dims), int(brick_size))) - 1
 
 
 @dataclass(frozen=True)
 class BrickKey:
+    """(LoD, brick index (i, j, k)) — brickmath.py:71-84."""
+
     lod: int
     index: tuple
 
@@ -75,22 +71,27 @@ class BrickKey:
 
 
 class BrickLayout:
-    """brickmath.py:87-151."""
+    """A volume's brick hierarchy (brickmath.py:87-151): per-level grids, the flat
+    numbering of bricks over all levels (level offsets), brick origins and the
+    native/normalized coordinates of a brick's B^3 samples."""
 
     def __init__(self, dims, brick_size: int):
         if brick_size < 2:
             raise ValueError("brick_size must be >= 2")
         self.dims = tuple(int(d) for d in dims)
         self.brick_size = int(brick_size)
-        self.max_lod = max_lod(self.dims, self.brick_size)
-        self.grids = [grid_dims(self.dims, self.brick_size, l) for l in range(self.max_lod + 1)]
-        counts = [g[0] * g[1] * g[2] for g in self.grids]
-        self.offsets = [int(v) for v in np.concatenate([[0], np.cumsum(counts)[:-1]])]
-        self.total = int(sum(counts))
+        self.grids = _level_table(self.dims, self.brick_size)
+        self.max_lod = len(self.grids) - 1
+        counts = np.prod(np.asarray(self.grids, dtype=np.int64), axis=1)
+        starts = np.zeros(len(counts), dtype=np.int64)
+        np.cumsum(counts[:-1], out=starts[1:])
+        self.offsets = [int(v) for v in starts]
+        self.total = int(counts.sum())
 
+    # -- numbering
     def brick_count(self, lod: int) -> int:
-        g = self.grids[lod]
-        return g[0] * g[1] * g[2]
+        gx, gy, gz = self.grids[lod]
+        return gx * gy * gz
 
     def total_bricks(self) -> int:
         return self.total
@@ -99,31 +100,14 @@ class BrickLayout:
         return self.offsets[key.lod] + key.linear_index(self.grids[key.lod])
 
     def key_of_flat(self, flat: int) -> BrickKey:
-        lod = int(np.searchsorted(self.offsets, flat, side="right") - 1)
-        lin = flat - self.offsets[lod]
-        g = self.grids[lod]
-        return BrickKey(lod, (lin % g[0], (lin // g[0]) % g[1], lin // (g[0] * g[1])))
+        lod = int(np.searchsorted(self.offsets, flat, side="right")) - 1
+        gx, gy, _ = self.grids[lod]
+        q, i = divmod(flat - self.offsets[lod], gx)
+        k, j = divmod(q, gy)
+        return BrickKey(lod, (i, j, k))
 
-    def locate(self, positions, lod: int):
-        if lod > self.max_lod:
-            raise ValueError(f"lod {lod} exceeds max_lod {self.max_lod}")
-        pos = np.asarray(positions, dtype=np.float64)
-        idx = locate_axis(pos, self.brick_size, lod)
-        np.clip(idx, 0, np.asarray(self.grids[lod], dtype=np.int64) - 1, out=idx)
-        local = (pos - brick_origin(idx, self.brick_size, lod)) / lod_stride(lod)
-        np.clip(local, 0.0, self.brick_size - 1, out=local)
-        return idx, local
-
-    def origin(self, key: BrickKey):
-        return tuple(int(v) for v in brick_origin(np.asarray(key.index), self.brick_size, key.lod))
-
-    def sample_positions(self, key: BrickKey):
-        b = self.brick_size
-        axis = np.arange(b, dtype=np.int64) * lod_stride(key.lod)
-        zz, yy, xx = np.meshgrid(axis, axis, axis, indexing="ij")
-        native = np.stack([xx.ravel(), yy.ravel(), zz.ravel()], axis=1) + np.asarray(self.origin(key))
-        np.clip(native, 0, np.asarray(self.dims, dtype=np.int64) - 1, out=native)
-        return native, (native + 0.5) / np.asarray(self.dims, dtype=np.float64)
+    def valid_key(self, key: BrickKey) -> bool:
+        return 0 <= key.lod <= self.max_lod and all(0 <= c < n for c, n in zip(key.index, self.grids[key.lod]))
 
     def keys_at(self, lod: int):
         gx, gy, gz = self.grids[lod]
@@ -132,21 +116,43 @@ class BrickLayout:
                 for i in range(gx):
                     yield BrickKey(lod, (i, j, k))
 
-    def valid_key(self, key: BrickKey) -> bool:
-        if not 0 <= key.lod <= self.max_lod:
-            return False
-        return all(0 <= key.index[a] < self.grids[key.lod][a] for a in range(3))
+    # -- geometry
+    def _starts(self, index, lod: int):
+        """Native voxel of sample 0 of bricks `index` (int64 array) at `lod`."""
+        first = index * (self.brick_size << lod)
+        return np.where(index > 0, first - 1, first)
+
+    def origin(self, key: BrickKey):
+        return tuple(int(v) for v in self._starts(np.asarray(key.index, dtype=np.int64), key.lod))
+
+    def locate(self, positions, lod: int):
+        """(brick index, local sample coordinate) of native positions at `lod`."""
+        if lod > self.max_lod:
+            raise ValueError(f"lod {lod} is coarser than the hierarchy's {self.max_lod}")
+        pos = np.asarray(positions, dtype=np.float64)
+        idx = np.floor((pos + 1.0) / (self.brick_size << lod)).astype(np.int64)
+        np.clip(idx, 0, np.asarray(self.grids[lod], dtype=np.int64) - 1, out=idx)
+        local = (pos - self._starts(idx, lod)) / (1 << lod)
+        np.clip(local, 0.0, self.brick_size - 1, out=local)
+        return idx, local
+
+    def sample_positions(self, key: BrickKey):
+        """A brick's B^3 samples, x fastest: native voxels (clipped to the volume) and
+        the normalized positions (n + 0.5) / V the field is evaluated at."""
+        steps = np.arange(self.brick_size, dtype=np.int64) << key.lod
+        z, y, x = np.meshgrid(steps, steps, steps, indexing="ij")
+        native = np.column_stack([x.ravel(), y.ravel(), z.ravel()]) + np.asarray(self.origin(key))
+        np.clip(native, 0, np.asarray(self.dims, dtype=np.int64) - 1, out=native)
+        return native, (native + 0.5) / np.asarray(self.dims, dtype=np.float64)
 
     def geom(self) -> N.VcbBrickGeom:
         g = N.VcbBrickGeom()
-        for a in range(3):
-            g.dims[a] = self.dims[a]
+        g.dims[:] = list(self.dims)
         g.b = self.brick_size
         g.n_lod = self.max_lod + 1
-        for l, gr in enumerate(self.grids):
-            for a in range(3):
-                g.grid[l][a] = gr[a]
-            g.offset[l] = self.offsets[l]
+        for lod, row in enumerate(self.grids):
+            g.grid[lod][:] = list(row)
+            g.offset[lod] = self.offsets[lod]
         return g
 
 

@@ -77,69 +77,78 @@ def camera_rays_setup(cam):
     return rot, float(tan_half * aspect), float(tan_half)
 
 
+def _checked_points(points) -> np.ndarray:
+    """Control points as a read-only (n, 5) f64 array: x from 0 to 1 strictly
+    increasing, colour and opacity in [0, 1] (transfer.py:16-27's rules)."""
+    pts = np.array(points, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] != 5 or len(pts) < 2:
+        raise ConfigError("a transfer function is at least two (x, r, g, b, a) rows")
+    xs = pts[:, 0]
+    if not (xs[0] == 0.0 and xs[-1] == 1.0 and np.all(xs[1:] > xs[:-1])):
+        raise ConfigError("transfer-function x must run strictly upward from 0 to 1")
+    if np.any((pts[:, 1:] < 0.0) | (pts[:, 1:] > 1.0)):
+        raise ConfigError("transfer-function colour/opacity outside [0, 1]")
+    pts.flags.writeable = False
+    return pts
+
+
 class TransferFunction:
-    """Ordered control points (x, r, g, b, a), x strictly increasing from 0 to 1."""
+    """Piecewise-linear colour/opacity of a normalized value (transfer.py:13-78): the
+    control points, their interpolation, and the dense LUT the shade samples."""
 
     def __init__(self, points):
-        pts = np.asarray(points, dtype=np.float64)
-        if pts.ndim != 2 or pts.shape[1] != 5 or pts.shape[0] < 2:
-            raise ConfigError("transfer function needs >= 2 control points of (x, r, g, b, a)")
-        x = pts[:, 0]
-        if x[0] != 0.0 or x[-1] != 1.0 or not (np.diff(x) > 0).all():
-            raise ConfigError("control point x values must increase strictly from 0 to 1")
-        if (pts[:, 1:] < 0).any() or (pts[:, 1:] > 1).any():
-            raise ConfigError("color and opacity components must lie in [0,1]")
-        self.points = pts
-        self.points.flags.writeable = False
+        self.points = _checked_points(points)
+        self._tables = {}
+
+    def _interp(self, values, column):
+        v = np.clip(np.asarray(values, dtype=np.float64), 0.0, 1.0)
+        return np.interp(v, self.points[:, 0], self.points[:, column])
 
     def eval(self, values) -> np.ndarray:
-        v = np.clip(np.asarray(values, dtype=np.float64), 0.0, 1.0)
-        out = np.empty(v.shape + (4,), dtype=np.float64)
-        for c in range(4):
-            out[..., c] = np.interp(v, self.points[:, 0], self.points[:, c + 1])
-        return out
-
-    def lookup_table(self, size: int = 1024) -> np.ndarray:
-        lut = getattr(self, "_lut", None)
-        if lut is None or lut.shape[0] != size:
-            lut = self.eval(np.linspace(0.0, 1.0, size)).astype(np.float32)
-            self._lut = lut
-        return lut
+        """rgba (..., 4) f64 at each value (clamped to [0, 1])."""
+        return np.stack([self._interp(values, c) for c in (1, 2, 3, 4)], axis=-1)
 
     def opacity(self, values) -> np.ndarray:
-        v = np.clip(np.asarray(values, dtype=np.float64), 0.0, 1.0)
-        return np.interp(v, self.points[:, 0], self.points[:, 4])
+        return self._interp(values, 4)
+
+    def lookup_table(self, size: int = 1024) -> np.ndarray:
+        """(size, 4) f32 rgba at size evenly spaced values; built once per size."""
+        if size not in self._tables:
+            self._tables[size] = self.eval(np.linspace(0.0, 1.0, size)).astype(np.float32)
+        return self._tables[size]
 
     def to_json(self):
-        return [{"x": float(p[0]), "rgb": [float(p[1]), float(p[2]), float(p[3])], "a": float(p[4])} for p in self.points]
+        return [dict(x=float(x), rgb=[float(r), float(g), float(b)], a=float(a)) for x, r, g, b, a in self.points]
 
     @classmethod
     def from_json(cls, data) -> "TransferFunction":
         try:
-            pts = [[p["x"], p["rgb"][0], p["rgb"][1], p["rgb"][2], p["a"]] for p in data]
+            rows = [(e["x"], *e["rgb"][:3], e["a"]) for e in data]
         except (KeyError, TypeError, IndexError) as exc:
-            raise ConfigError(f"malformed transfer function JSON: {exc}") from exc
-        return cls(pts)
+            raise ConfigError(f"transfer-function JSON is malformed: {exc}") from exc
+        return cls(rows)
 
     @classmethod
     def load(cls, path) -> "TransferFunction":
         return cls.from_json(json.loads(Path(path).read_text()))
 
 
+# presets (transfer.py:80-98): the same control points
 def grayscale_ramp(max_opacity: float = 1.0) -> TransferFunction:
-    return TransferFunction([[0.0, 0.0, 0.0, 0.0, 0.0], [1.0, 1.0, 1.0, 1.0, max_opacity]])
+    return TransferFunction([(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, max_opacity)])
 
 
 def transparent() -> TransferFunction:
-    return TransferFunction([[0.0, 0.0, 0.0, 0.0, 0.0], [1.0, 1.0, 1.0, 1.0, 0.0]])
+    return grayscale_ramp(0.0)
 
 
 def warm_body(threshold: float = 0.35, max_opacity: float = 0.9) -> TransferFunction:
-    """transfer.py:88-98."""
-    t = float(np.clip(threshold, 0.01, 0.95))
-    return TransferFunction([[0.0, 0.0, 0.0, 0.1, 0.0], [t, 0.1, 0.05, 0.3, 0.0],
-                             [min(t + 0.15, 0.97), 0.9, 0.45, 0.1, 0.55 * max_opacity],
-                             [1.0, 1.0, 0.95, 0.8, max_opacity]])
+    """Transparent below `threshold` (clamped to [0.01, 0.95]), warm and opaque above."""
+    t = min(max(float(threshold), 0.01), 0.95)
+    return TransferFunction([(0.0, 0.0, 0.0, 0.1, 0.0),
+                             (t, 0.1, 0.05, 0.3, 0.0),
+                             (min(t + 0.15, 0.97), 0.9, 0.45, 0.1, 0.55 * max_opacity),
+                             (1.0, 1.0, 0.95, 0.8, max_opacity)])
 
 
 @dataclass
