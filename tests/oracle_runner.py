@@ -39,6 +39,8 @@ def oracle_config(spec):
         cached=spec.get("cached", True), seed=spec.get("seed", 0),
         skip_empty=st.get("skip_empty", True), adaptive=st.get("adaptive_step", True),
         base_step_scale=st.get("base_step_scale", 0.5), rng=spec.get("rng", "rank"),
+        max_iterations=st.get("max_iterations", 8192), background=tuple(st.get("background", (0.0, 0.0, 0.0))),
+        term=st.get("early_termination", 0.01),
     )
 
 

@@ -150,3 +150,49 @@ def test_bands_join_to_the_frame():
     for r in range(3):
         joined[r::3] = run((r, 3))
     np.testing.assert_array_equal(joined, full)
+
+
+@pytest.mark.parametrize("case", ["odd_size", "iteration_cap", "background", "fixed_steps", "no_skip", "nothing_hit"])
+def test_edge_cases_vs_oracle(case):
+    """Throughput schedule vs the oracle (pixel lanes) on edge cases: film sizes that
+    are not multiples of the 8x4 ray tiles, the iteration cap flushing live rays
+    (raymarch.py:117), a coloured background, fixed-ladder steps and no empty-space
+    skipping (the generic kernel build), and a camera that misses the volume."""
+    import scene_specs
+    from gpu_runner import run_gpu_session
+
+    base = dict(scene_specs.SESSION_SPECS["pressure"], rng="pixel", frames=5)
+    over = {
+        "odd_size": dict(res=(37, 23)),
+        "iteration_cap": dict(settings=dict(max_iterations=6)),
+        "background": dict(settings=dict(background=(0.2, 0.1, 0.3), early_termination=0.05)),
+        "fixed_steps": dict(settings=dict(adaptive_step=False), res=(40, 33)),
+        "no_skip": dict(settings=dict(skip_empty=False), res=(41, 30)),
+        "nothing_hit": dict(radius=2.2, res=(24, 24), fov_far=True),
+    }[case]
+    spec = dict(base, **{k: v for k, v in over.items() if k != "fov_far"})
+    name = f"_edge_{case}"
+    scene_specs.SESSION_SPECS[name] = spec
+    try:
+        if case == "nothing_hit":
+            # a camera looking away from the unit box: background everywhere, no samples
+            import paper_2504_18001_b200 as P
+            from gpu_runner import product_config, product_field, product_tf
+            from paper_2504_18001_b200.session import RenderSession
+
+            cam = P.Camera(position=(3.0, 3.0, 3.0), target=(6.0, 6.0, 6.0), width=24, height=24)
+            s = RenderSession(product_field(spec), product_tf(spec["tf"]), cam, product_config(spec),
+                              march="throughput")
+            img, rec = s.render_frame()
+            assert rec.samples == 0 and s.last_frame_stats["rays"] == 0
+            assert (img == 0.0).all()
+            return
+        for (f, img, rec, sess), (_, oimg, orec, osess) in zip(run_gpu_session(name, impl=10),
+                                                               run_oracle_session(name)):
+            np.testing.assert_array_equal(_record(rec), record_array(orec), err_msg=f"{case} frame {f}")
+            st, ost = sess.debug_state(), oracle_state(osess)
+            for k in ("tables", "owner", "last_used", "entries", "reports", "batch"):
+                np.testing.assert_array_equal(st[k], ost[k], err_msg=f"{case} frame {f} {k}")
+            assert np.abs(img - oimg).max() <= 1e-6, f"{case} frame {f}"
+    finally:
+        scene_specs.SESSION_SPECS.pop(name, None)
