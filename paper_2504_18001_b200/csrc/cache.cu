@@ -244,7 +244,50 @@ __global__ void __launch_bounds__(kSelThreads) k_insert(VcbMaintParams P, MaintW
     }
     if (threadIdx.x == 0) n_lru_s = n_lru;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (n <= free_left && n <= kSelThreads) {
+        // the free list covers the batch: no eviction, so entries do not interact; every
+        // entry at once: a mapped key is refreshed in place (mrpd.py:240-243), a new key
+        // takes the next free slot in batch order (pool.py:55-58)
+        __shared__ int warp_new[kSelThreads / 32];
+        __shared__ int n_new_s;
+        const int i = threadIdx.x, lane = i & 31, wid = i >> 5;
+        long long key = -1;
+        int existing = -1;
+        if (i < n) {
+            key = P.staged_keys[i];
+            existing = P.table[key];
+        }
+        const bool fresh = i < n && existing < 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+        if (lane == 0) warp_new[wid] = __popc(bal);
+        __syncthreads();
+        int before = __popc(bal & ((1u << lane) - 1u));
+        for (int q = 0; q < wid; q++) before += warp_new[q];
+        if (i == 0) {
+            int t = 0;
+            for (int q = 0; q < kSelThreads / 32; q++) t += warp_new[q];
+            n_new_s = t;
+        }
+        if (i < n) {
+            const int slot = fresh ? (int)(nf0 + before) : existing;
+            if (fresh) {
+                const long long old = P.owner[slot];  // a free slot: unowned (-1)
+                if (old >= 0) P.table[old] = -1;
+                P.owner[slot] = key;
+                P.table[key] = slot;
+            }
+            P.last_used[slot] = f;
+            w.assign[i] = slot;
+        }
+        __syncthreads();
+        if (i == 0) {
+            st->next_free = nf0 + n_new_s;
+            st->bricks_loaded = n;
+            st->deferred = 0;
+            st->inserted = n_new_s;
+            st->loaded_total += n_new_s;
+        }
+    } else if (threadIdx.x == 0) {
         long long next_free = nf0, lp = 0, loaded = 0, deferred = 0, inserted = 0;
         for (long long i = 0; i < n; i++) {
             const long long key = P.staged_keys[i];
