@@ -118,6 +118,10 @@ class RenderSession:
         self._dstream = torch.cuda.Stream(self.device) if (config.loader == "thread" and config.cached) else None
         self._cstream = torch.cuda.Stream(self.device)  # device-to-host image copies
         self._ev_image = torch.cuda.Event()
+        # this session's own timing events (the library's per-thread ones would be shared
+        # by every session driven from the same thread)
+        self._ev_t0, self._ev_t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self._timed_launches = 0
         self._ev_decoded = None
 
     MARCH_SCHEDULES = {"parity": 0, "throughput": 10}
@@ -387,7 +391,12 @@ class RenderSession:
                 q = self._pt_params(p)
                 N.call("vcb_pathtrace_frame", C.byref(p), C.byref(q), stream_ptr(self.stream))
             else:
+                if self.timing:
+                    self._ev_t0.record(self.stream)
                 N.call("vcb_march_frame", C.byref(p), stream_ptr(self.stream))
+                if self.timing:
+                    self._ev_t1.record(self.stream)
+                    self._timed_launches = N.load().vcb_last_launch_count()
             # the image is final here: a host copy can overlap the maintenance below
             self._ev_image.record(self.stream)
             if self.cache is not None:
@@ -485,12 +494,10 @@ class RenderSession:
             self._pin_free.append(torch.empty(shape, dtype=torch.float32, pin_memory=True))
 
     def march_kernel_time(self):
-        """(ms, launches) of the ray-march kernel in the last timing=True frame."""
-        ms = C.c_double(0.0)
-        n = C.c_int64(0)
-        it = int(self.last_frame_stats.get("iterations", 0)) + 1
-        N.call("vcb_march_timing", it, C.byref(ms), C.byref(n))
-        return ms.value, n.value
+        """(ms, frames) of the frame-kernel call (ray setup + march) in the last
+        timing=True frame, from this session's CUDA events on its stream."""
+        self._ev_t1.synchronize()
+        return self._ev_t0.elapsed_time(self._ev_t1), 1
 
     def frame_trace(self):
         """Per-iteration diagnostics of the last timing=True frame (default schedule):
