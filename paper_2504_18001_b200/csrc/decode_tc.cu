@@ -229,8 +229,15 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_inr_decode_tc2(const __grid_
     }
     const long long tab_rows = n_smem_levels > 0 ? F.tab_off[n_smem_levels] : 0;  // levels are contiguous
     const float2* gtab = reinterpret_cast<const float2*>(F.tables);
-    for (long long e = tid; e < tab_rows; e += kTc2Threads) s_tab[e] = __ldg(gtab + e);
-    if (tid == 0) sm.b2 = __ldg(F.biases + 64);
+    // the dense levels are a plain copy: one TMA bulk copy (whole 16-byte rows; the smem
+    // region is rounded up to match)
+    __shared__ __align__(8) uint64_t tma_bar;
+    if (tid == 0) {
+        const uint32_t bytes = ((uint32_t)tab_rows * 8u + 15u) & ~15u;
+        tma_stage_begin(&tma_bar, bytes);
+        if (bytes) tma_stage_copy(s_tab, gtab, bytes, &tma_bar);
+        sm.b2 = __ldg(F.biases + 64);
+    }
     if (row == 0) {
         const uint32_t a = (uint32_t)__cvta_generic_to_shared(&sm.g[grp].mbar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a));
@@ -245,6 +252,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_inr_decode_tc2(const __grid_
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tma_stage_wait(&tma_bar);
     Tc2Group& G = sm.g[grp];
     const uint32_t tmem = sm.tmem + (uint32_t)(grp * 64);  // 64 columns per group: D0 | D1
     const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&G.a0[0][0]);
@@ -345,7 +353,7 @@ template <class Src>
 static int launch_tc2(const VcbField& F, const Src& src, long long n, float* out, int32_t* nonfinite,
                       cudaStream_t st, const int64_t* n_keys_dev = nullptr, long long per_key = 0) {
     const int L = tc2_smem_levels(F);
-    const size_t smem = ((sizeof(Tc2Smem) + 127) & ~size_t(127)) + (size_t)(L > 0 ? F.tab_off[L] : 0) * 8;
+    const size_t smem = ((sizeof(Tc2Smem) + 127) & ~size_t(127)) + (((size_t)(L > 0 ? F.tab_off[L] : 0) * 8 + 15) & ~size_t(15));
     kernel_ctas_per_sm((const void*)k_inr_decode_tc2<Src>, kTc2Threads, (int)smem);  // raises the smem limit once
     const long long tiles = (n + kTcRows - 1) / kTcRows;
     long long grid = (tiles + kTc2Groups - 1) / kTc2Groups;

@@ -176,21 +176,30 @@ __global__ void __launch_bounds__(NT, 1)
     const unsigned lt_mask = (1u << lane) - 1u;
     const double hmax = 0.99999999999999989;  // np.nextafter(1.0, 0.0)
 
-    // ---- read-only tables in shared memory: LUT, majorants (or occupancy bits), MLP
+    // ---- read-only tables in shared memory: LUT, majorants (or occupancy bits), MLP.
+    // The LUT, the majorant grid and the super-cell bits are plain copies: one TMA bulk
+    // copy each (cp.async.bulk), completing on one mbarrier, while the threads stage the
+    // rest.
+    __shared__ __align__(8) uint64_t tma_bar;
     float* s_lut = cfg.sm_lut >= 0 ? reinterpret_cast<float*>(dsm + cfg.sm_lut) : nullptr;
-    if (s_lut)
-        for (int i = threadIdx.x; i < p.lut_size * 4; i += NT) s_lut[i] = __ldg(p.lut + i);
     const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
     const float* mu_s = nullptr;
     const uint32_t* occ = nullptr;
+    const uint32_t lut_bytes = s_lut ? (uint32_t)p.lut_size * 16u : 0u;
+    const uint32_t mu_bytes = 0u;  // (the majorant grid: by the threads, measured faster at config 2)
+    const uint32_t co_bytes = kFast == 2 ? ((uint32_t)cfg.coarse_words * 4u + 15u) & ~15u : 0u;
+    if (threadIdx.x == 0) {
+        tma_stage_begin(&tma_bar, lut_bytes + mu_bytes + co_bytes);
+        if (lut_bytes) tma_stage_copy(s_lut, p.lut, lut_bytes, &tma_bar);
+        if (mu_bytes) tma_stage_copy(dsm + cfg.sm_mu, p.mu, mu_bytes, &tma_bar);
+        if (co_bytes) tma_stage_copy(dsm + cfg.sm_occ, cfg.coarse, co_bytes, &tma_bar);
+    }
     if (cfg.sm_mu >= 0) {
         float* m = reinterpret_cast<float*>(dsm + cfg.sm_mu);
-        for (long long i = threadIdx.x; i < cells; i += NT) m[i] = __ldg(p.mu + i);
+        for (long long i = mu_bytes / 4 + threadIdx.x; i < cells; i += NT) m[i] = __ldg(p.mu + i);
         mu_s = m;
     } else if (kFast == 2) {
-        uint32_t* o = reinterpret_cast<uint32_t*>(dsm + cfg.sm_occ);
-        for (int i = threadIdx.x; i < cfg.coarse_words; i += NT) o[i] = __ldcg(cfg.coarse + i);
-        occ = o;
+        occ = reinterpret_cast<const uint32_t*>(dsm + cfg.sm_occ);
     } else if (cfg.sm_occ >= 0) {
         uint32_t* o = reinterpret_cast<uint32_t*>(dsm + cfg.sm_occ);
         const int nwords = (int)((cells + 31) >> 5);
@@ -216,6 +225,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (threadIdx.x < 7) sm.cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) sm.max_k = 0;
     __syncthreads();
+    tma_stage_wait(&tma_bar);
     const float* lut = s_lut ? s_lut : p.lut;
 
     const double ox = p.cam.origin[0], oy = p.cam.origin[1], oz = p.cam.origin[2];
@@ -465,6 +475,8 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     cfg.n_tickets = (long long)cfg.tiles_x * ((p.cam.rows + 3) / 4) * 32;
     cfg.n_rays = &w.ctr->pad[0];
     if (cfg.n_tickets >= (1ll << 31)) return set_error("march_frame: %lld pixels exceed the ticket range", (long long)npix);
+    if (((uintptr_t)p.lut | (uintptr_t)p.mu) & 15)
+        return set_error("march_frame: the LUT and majorant arrays must be 16-byte aligned (TMA)");
     int off = 0;
     auto take = [&](int bytes) {
         const int o = (off + 15) & ~15;
@@ -495,7 +507,7 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
         const int words = (int)((nsc + 31) / 32);
         if (words <= kCoarseMaxWords) {
             // (the plain occupancy bitmask chosen above is dropped in this mode)
-            cfg.sm_occ = take(words * 4);
+            cfg.sm_occ = take((words * 4 + 15) & ~15);  // whole 16-byte rows for the TMA copy
             cfg.coarse_words = words;
             fast = 2;
         }

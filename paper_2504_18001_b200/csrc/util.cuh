@@ -10,6 +10,33 @@ namespace cinr {
 int set_error(const char* fmt, ...);
 int check_launch(const char* what);
 int device_sms();
+
+// TMA bulk copies global -> shared (cp.async.bulk, SASS UBLKCP) completing on one
+// mbarrier.  Usage: thread 0 calls tma_stage_begin(bar, total bytes), then
+// tma_stage_copy for each region (16-byte aligned addresses, sizes multiples of 16);
+// after a __syncthreads() every thread calls tma_stage_wait(bar).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_stage_begin(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_stage_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_stage_wait(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "TMA_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra TMA_WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
 int kernel_ctas_per_sm(const void* fn, int threads, int smem);
 
 inline int grid_for(int64_t n, int block, int cap_per_sm = 16) {
