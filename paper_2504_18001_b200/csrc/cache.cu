@@ -119,15 +119,48 @@ __global__ void k_report(VcbMaintParams P, MaintWs w) {
     }
 }
 
-// Smallest-m selection of unique 64-bit keys by one CTA: MSB-first radix select
-// with 8-bit digits, then the <= threshold keys are gathered and rank-sorted.
+// Smallest-m selection of unique 64-bit keys by one CTA: one pass finds the
+// candidates' key range, then an MSB-first radix select with 11-bit digits over the
+// key offsets (k - kmin: the spread, not the 64-bit width, sets the pass count --
+// 2-3 passes for the LRU and request-table keys), the digit holding the m-th key
+// found by a block scan of the histogram; the <= threshold keys are gathered and
+// rank-sorted.
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;  // = 2 * kSelThreads
+static_assert(kBins == 2 * kSelThreads, "two histogram bins per thread");
+
 struct SelSmem {
-    unsigned int hist[256];
-    unsigned long long prefix, mask;
-    long long remaining;
+    unsigned int hist[kBins];
+    unsigned int warp_sum[kSelThreads / 32];
+    unsigned long long prefix, mask, kmin, kmax;
+    long long remaining, ncand;
     int n_out;
     long long out[kMaxSel];
 };
+
+// exclusive block scan of one value per thread (blockDim = kSelThreads)
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_sum) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned t = warp_sum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_sum[lane] = t - warp_sum[lane];  // exclusive warp offsets
+    }
+    __syncthreads();
+    return x - v + warp_sum[wid];
+}
 
 template <typename KeyFn>
 __device__ int block_select_smallest(KeyFn key_of, long long n, int m, SelSmem& s, long long* sorted_out) {
@@ -137,56 +170,68 @@ __device__ int block_select_smallest(KeyFn key_of, long long n, int m, SelSmem& 
         s.mask = 0;
         s.remaining = m;
         s.n_out = 0;
-    }
-    // count candidates and find the key bit-width
-    __shared__ unsigned long long kmax_s;
-    __shared__ long long ncand_s;
-    if (threadIdx.x == 0) {
-        kmax_s = 0;
-        ncand_s = 0;
+        s.kmin = ~0ull;
+        s.kmax = 0;
+        s.ncand = 0;
     }
     __syncthreads();
-    unsigned long long kmax = 0;
+    unsigned long long kmin = ~0ull, kmax = 0;
     long long nc = 0;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
         unsigned long long k;
         if (key_of(i, k)) {
             kmax = k > kmax ? k : kmax;
+            kmin = k < kmin ? k : kmin;
             nc++;
         }
     }
-    atomicMax(&kmax_s, kmax);
-    atomicAdd((unsigned long long*)&ncand_s, (unsigned long long)nc);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmax, o), b = __shfl_xor_sync(0xffffffffu, kmin, o);
+        kmax = a > kmax ? a : kmax;
+        kmin = b < kmin ? b : kmin;
+        nc += __shfl_xor_sync(0xffffffffu, nc, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&s.kmax, kmax);
+        atomicMin(&s.kmin, kmin);
+        atomicAdd((unsigned long long*)&s.ncand, (unsigned long long)nc);
+    }
     __syncthreads();
-    const long long ncand = ncand_s;
+    const long long ncand = s.ncand;
+    const unsigned long long base = s.kmin;
     unsigned long long thresh = ~0ull;
     if (ncand > m) {
-        int top = 64 - __clzll((long long)kmax_s);
-        int shift = ((top + 7) / 8) * 8;
+        const unsigned long long span = s.kmax - base;  // > 0: keys are unique, ncand >= 2
+        const int bits = 64 - __clzll((long long)span);
+        int shift = ((bits + kDigitBits - 1) / kDigitBits) * kDigitBits;
         while (shift > 0) {
-            shift -= 8;
-            for (int i = threadIdx.x; i < 256; i += blockDim.x) s.hist[i] = 0;
+            shift -= kDigitBits;
+            s.hist[threadIdx.x] = 0;
+            s.hist[threadIdx.x + kSelThreads] = 0;
             __syncthreads();
             const unsigned long long pf = s.prefix, mk = s.mask;
+            const long long rem = s.remaining;
             for (long long i = threadIdx.x; i < n; i += blockDim.x) {
                 unsigned long long k;
-                if (key_of(i, k) && (k & mk) == pf) atomicAdd(&s.hist[(k >> shift) & 255ull], 1u);
+                if (key_of(i, k)) {
+                    const unsigned long long r = k - base;
+                    if ((r & mk) == pf) atomicAdd(&s.hist[(r >> shift) & (kBins - 1)], 1u);
+                }
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                long long rem = s.remaining;
-                int d = 0;
-                for (; d < 256; d++) {
-                    if ((long long)s.hist[d] >= rem) break;
-                    rem -= s.hist[d];
-                }
-                s.remaining = rem;
-                s.prefix = pf | ((unsigned long long)d << shift);
-                s.mask = mk | (255ull << shift);
+            const unsigned a = s.hist[2 * threadIdx.x], b = s.hist[2 * threadIdx.x + 1];
+            const long long ex = block_excl_scan(a + b, s.warp_sum);
+            // exactly one thread's pair of bins holds the rem-th key
+            if (ex < rem && ex + a + b >= rem) {
+                const bool first = ex + a >= rem;
+                const unsigned long long d = 2ull * threadIdx.x + (first ? 0 : 1);
+                s.remaining = first ? rem - ex : rem - ex - a;
+                s.prefix = pf | (d << shift);
+                s.mask = mk | ((unsigned long long)(kBins - 1) << shift);
             }
             __syncthreads();
         }
-        thresh = s.prefix;  // the m-th smallest key
+        thresh = base + s.prefix;  // the m-th smallest key
     }
     __syncthreads();
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
@@ -226,6 +271,19 @@ __global__ void __launch_bounds__(kSelThreads) k_insert(VcbMaintParams P, MaintW
     const long long f = P.session_frame;
     const long long nf0 = st->next_free;
     const long long free_left = P.slots - nf0;
+    // entries already mapped are refreshed in place (mrpd.py:240-243); their slots are
+    // stashed in w.assign (each thread revisits only its own entries below)
+    __shared__ int n_exist_s;
+    if (threadIdx.x == 0) n_exist_s = 0;
+    __syncthreads();
+    int ne = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const int e = P.table[P.staged_keys[i]];
+        w.assign[i] = e;
+        ne += e >= 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, o);
+    if ((threadIdx.x & 31) == 0 && ne) atomicAdd(&n_exist_s, ne);
     // LRU candidates only matter when the free list cannot cover the batch
     long long n_lru = 0;
     if (n > free_left) {
@@ -244,48 +302,46 @@ __global__ void __launch_bounds__(kSelThreads) k_insert(VcbMaintParams P, MaintW
     }
     if (threadIdx.x == 0) n_lru_s = n_lru;
     __syncthreads();
-    if (n <= free_left && n <= kSelThreads) {
-        // the free list covers the batch: no eviction, so entries do not interact; every
-        // entry at once: a mapped key is refreshed in place (mrpd.py:240-243), a new key
-        // takes the next free slot in batch order (pool.py:55-58)
-        __shared__ int warp_new[kSelThreads / 32];
-        __shared__ int n_new_s;
-        const int i = threadIdx.x, lane = i & 31, wid = i >> 5;
-        long long key = -1;
-        int existing = -1;
-        if (i < n) {
-            key = P.staged_keys[i];
-            existing = P.table[key];
-        }
-        const bool fresh = i < n && existing < 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, fresh);
-        if (lane == 0) warp_new[wid] = __popc(bal);
-        __syncthreads();
-        int before = __popc(bal & ((1u << lane) - 1u));
-        for (int q = 0; q < wid; q++) before += warp_new[q];
-        if (i == 0) {
-            int t = 0;
-            for (int q = 0; q < kSelThreads / 32; q++) t += warp_new[q];
-            n_new_s = t;
-        }
-        if (i < n) {
-            const int slot = fresh ? (int)(nf0 + before) : existing;
-            if (fresh) {
-                const long long old = P.owner[slot];  // a free slot: unowned (-1)
-                if (old >= 0) P.table[old] = -1;
-                P.owner[slot] = key;
-                P.table[key] = slot;
+    if (n_exist_s == 0 || n <= free_left) {
+        // no refreshed slot can be an LRU pick, so entries do not interact: the r-th new
+        // key (batch order) takes the r-th free slot (pool.py:55-58), then the r-th
+        // oldest (last_used, slot) (pool.py:59-62), else it is deferred
+        __shared__ int chunk_new_s;
+        long long new_before = 0;
+        for (long long c0 = 0; c0 < n; c0 += blockDim.x) {
+            const long long i = c0 + threadIdx.x;
+            const int existing = i < n ? w.assign[i] : 0;
+            const bool fresh = i < n && existing < 0;
+            const unsigned rk = block_excl_scan(fresh ? 1u : 0u, s.warp_sum);
+            if (threadIdx.x == blockDim.x - 1) chunk_new_s = (int)rk + (fresh ? 1 : 0);
+            if (i < n) {
+                int slot = existing;
+                if (fresh) {
+                    const long long r = new_before + rk;
+                    const long long key = P.staged_keys[i];
+                    slot = r < free_left ? (int)(nf0 + r) : (r - free_left < n_lru ? (int)w.lru[r - free_left] : -1);
+                    if (slot >= 0) {
+                        const long long old = P.owner[slot];
+                        if (old >= 0) P.table[old] = -1;
+                        P.owner[slot] = key;
+                        P.table[key] = slot;
+                    }
+                }
+                if (slot >= 0) P.last_used[slot] = f;
+                w.assign[i] = slot;
             }
-            P.last_used[slot] = f;
-            w.assign[i] = slot;
+            __syncthreads();
+            new_before += chunk_new_s;
+            __syncthreads();
         }
-        __syncthreads();
-        if (i == 0) {
-            st->next_free = nf0 + n_new_s;
-            st->bricks_loaded = n;
-            st->deferred = 0;
-            st->inserted = n_new_s;
-            st->loaded_total += n_new_s;
+        if (threadIdx.x == 0) {
+            const long long from_free = new_before < free_left ? new_before : free_left;
+            const long long from_lru = new_before - from_free < n_lru ? new_before - from_free : n_lru;
+            st->next_free = nf0 + from_free;
+            st->bricks_loaded = (n - new_before) + from_free + from_lru;
+            st->deferred = new_before - from_free - from_lru;
+            st->inserted = from_free + from_lru;
+            st->loaded_total += from_free + from_lru;
         }
     } else if (threadIdx.x == 0) {
         long long next_free = nf0, lp = 0, loaded = 0, deferred = 0, inserted = 0;
