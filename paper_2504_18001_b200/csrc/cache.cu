@@ -67,6 +67,8 @@ __device__ __forceinline__ int lod_of(const VcbBrickGeom& G, long long flat) {
 }
 
 __global__ void k_maint_gate(VcbMaintParams P, MaintWs w) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) w.ctr[i] = 0;  // [0] n_pending, [1] n_reports (64 B)
     w.nonfinite[0] = 0;
     w.nonfinite[1] = (P.frame_stats != nullptr && P.frame_stats->nonfinite != 0) ? 1 : 0;
     *w.n_dec() = 0;
@@ -593,7 +595,6 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     MaintWs w;
     int64_t need = maint_ws_layout(P.total, P.workspace, &w);
     if (need > P.workspace_bytes) return set_error("maintenance: workspace too small");
-    cudaMemsetAsync(w.ctr, 0, 64, st);
     // the decode flag is per maintenance (set by this call's decode, read by k_post_decode);
     // the workspace comes uninitialised from the caller.  The gate also reads the frame's
     // non-finite flag: a failed frame skips every step below on the device.

@@ -472,7 +472,9 @@ static unsigned long long* mapped_live(int n, unsigned long long** dev) {
 extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
     const VcbFrameParams& p = *pp;
     cudaStream_t st = (cudaStream_t)stream_;
-    cudaMemsetAsync(p.stats, 0, sizeof(VcbFrameStats), st);  // this frame's counters
+    // this frame's counters (the ray path's setup kernel clears them itself)
+    const bool ray_path = p.impl >= 10 && p.impl <= 14 && (int64_t)p.cam.width * p.cam.rows > 0;
+    if (!ray_path) cudaMemsetAsync(p.stats, 0, sizeof(VcbFrameStats), st);
     if (p.impl != 1) {
         if ((int64_t)p.cam.width * p.cam.rows == 0) return 0;
         g_ev_used = 0;

@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(256) k_ray_setup(const __grid_constant__ VcbFr
     const int lane = threadIdx.x & 31;
     const int W = p.cam.width, H = p.cam.height, rows = p.cam.rows;
     const float4 bgv = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+    if (blockIdx.x == 0 && threadIdx.x < sizeof(VcbFrameStats) / 8)
+        reinterpret_cast<long long*>(p.stats)[threadIdx.x] = 0;  // the march accumulates after this kernel
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long t0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < cfg.n_tickets; t0 += stride) {
         const long long t = t0 + lane;

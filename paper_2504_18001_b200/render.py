@@ -7,6 +7,7 @@ numpy expressions exactly so GPU rays match the reference bit for bit.
 from __future__ import annotations
 
 import json
+import math
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -75,6 +76,39 @@ def camera_rays_setup(cam):
     tan_half = np.tan(np.radians(cam.fov_y) / 2.0)
     aspect = cam.width / cam.height
     return rot, float(tan_half * aspect), float(tan_half)
+
+
+_TAN_HALF = {}
+
+
+def _norm3(v) -> float:
+    """np.linalg.norm of a 3-vector: numpy computes sqrt(x.dot(x)) (linalg.norm, ord
+    None), so this is that expression without norm's argument handling."""
+    a = np.array(v)
+    return math.sqrt(a.dot(a))
+
+
+def camera_frame_setup(cam):
+    """camera_rays_setup + the camera's distance to the unit box, flat, for the per-frame
+    kernel parameters: (origin3, rot9 row-major, tan_h, tan_v, box_distance).  The
+    same operations as camera_basis / camera_rays_setup / point_to_unit_box
+    (sampler.py:283-285), bit for bit (tests/test_host_cpu.py); tan(fov/2) is cached per
+    fov (np.tan, as before)."""
+    p, t, u = cam.position, cam.target, cam.up
+    p0, p1, p2 = float(p[0]), float(p[1]), float(p[2])
+    fwd = (float(t[0]) - p0, float(t[1]) - p1, float(t[2]) - p2)
+    n = _norm3(fwd)
+    fwd = (fwd[0] / n, fwd[1] / n, fwd[2] / n)
+    right = _cross(fwd, (float(u[0]), float(u[1]), float(u[2])))
+    n = _norm3(right)
+    right = (right[0] / n, right[1] / n, right[2] / n)
+    up = _cross(right, fwd)
+    th = _TAN_HALF.get(cam.fov_y)
+    if th is None:
+        th = _TAN_HALF.setdefault(cam.fov_y, float(np.tan(np.radians(cam.fov_y) / 2.0)))
+    gap = (max(max(-p0, p0 - 1.0), 0.0), max(max(-p1, p1 - 1.0), 0.0), max(max(-p2, p2 - 1.0), 0.0))
+    return ((p0, p1, p2), (right[0], up[0], fwd[0], right[1], up[1], fwd[1], right[2], up[2], fwd[2]),
+            float(th * (cam.width / cam.height)), th, _norm3(gap))
 
 
 def _checked_points(points) -> np.ndarray:

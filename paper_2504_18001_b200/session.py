@@ -27,9 +27,9 @@ from . import macrocell
 from .cache import CacheConfig, DeviceCache
 from .device import device_field, ptr, require_cuda, stream_ptr
 from .errors import ConfigError, ModelCorruptError, RenderError
-from .render import PT_MAX_WALK, RenderSettings, base_step, camera_rays_setup, pcg64_seeded_state
+from .render import PT_MAX_WALK, RenderSettings, base_step, camera_frame_setup, pcg64_seeded_state
 from .sampler import (MASK64, MODES, LodPolicy, effective_lod_scale, force_max_scale, frame_rng_base,
-                      point_to_unit_box, splitmix64)
+                      splitmix64)
 from .scheduler import SchedulerConfig
 
 
@@ -101,9 +101,17 @@ class RenderSession:
         self.mode = config.mode
         self._ws = None
         self._img = None
-        self._stats = torch.zeros(C.sizeof(N.VcbFrameStats) // 8, dtype=torch.int64, device=self.device)
-        self._host_stats = torch.zeros(self._stats.numel() + (self.cache.state.numel() if self.cache else 0),
-                                       dtype=torch.int64).pin_memory()
+        # the frame's counters and the cache's state words share one device buffer, so the
+        # FrameRecord needs a single device-to-host copy per frame
+        ns = C.sizeof(N.VcbFrameStats) // 8
+        self._dev_stats = torch.zeros(ns + (self.cache.state.numel() if self.cache else 0), dtype=torch.int64,
+                                      device=self.device)
+        self._stats = self._dev_stats[:ns]
+        if self.cache is not None:
+            with torch.cuda.stream(self.stream):
+                self._dev_stats[ns:].copy_(self.cache.state)
+            self.cache.state = self._dev_stats[ns:]
+        self._host_stats = torch.zeros(self._dev_stats.numel(), dtype=torch.int64).pin_memory()
         self.last_frame_stats = {}
         self.timing = False  # CUDA-event time the frame kernel (bench)
         self.trace = False  # record the per-iteration trace (diagnostics)
@@ -282,13 +290,13 @@ class RenderSession:
             self._tmpl_key = key
         p = N.VcbFrameParams.from_buffer_copy(self._tmpl)
         # per frame: the camera pose, the LoD scale of the preload ramp, the clocks
-        rot, tan_h, tan_v = camera_rays_setup(cam)
-        p.cam.origin[:] = [float(x) for x in cam.position]
-        p.cam.rot[:] = [float(x) for x in rot.ravel()]
+        origin, rot, tan_h, tan_v, box_dist = camera_frame_setup(cam)
+        p.cam.origin[:] = origin
+        p.cam.rot[:] = rot
         p.cam.tan_h, p.cam.tan_v = tan_h, tan_v
         c = self.cache
         if c is not None:
-            force = force_max_scale(c.max_lod, point_to_unit_box(np.asarray(cam.position, dtype=np.float64)))
+            force = force_max_scale(c.max_lod, box_dist)
             p.probe.lod_scale = effective_lod_scale(cfg.policy, self.frame, force)
             p.cache_frame = c.frame
         p.rng_base = frame_rng_base(cfg.seed, self.frame)
@@ -413,11 +421,8 @@ class RenderSession:
                     self.cache.decode(self._dstream)
                     self._ev_decoded = torch.cuda.Event()
                     self._ev_decoded.record(self._dstream)
-            # one small D2H for the FrameRecord counters
-            ns = self._stats.numel()
-            self._host_stats[:ns].copy_(self._stats, non_blocking=True)
-            if self.cache is not None:
-                self._host_stats[ns:].copy_(self.cache.state, non_blocking=True)
+            # one small D2H for the FrameRecord counters and the cache state
+            self._host_stats.copy_(self._dev_stats, non_blocking=True)
         return img
 
     def collect_record(self, t0: float) -> FrameRecord:

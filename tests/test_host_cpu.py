@@ -122,6 +122,40 @@ def test_camera_setup_matches_reference_raygen_inputs():
     assert isinstance(cam, P.Camera)
 
 
+def test_camera_frame_setup_equals_array_forms():
+    """The flat per-frame camera setup the session uses equals camera_rays_setup and
+    point_to_unit_box bit for bit (random poses, ups, fovs, aspect ratios) and the
+    reference's raygen inputs."""
+    from paper_2504_18001_b200.errors import ConfigError
+    from paper_2504_18001_b200.harness import OrbitTrajectory
+    from paper_2504_18001_b200.render import Camera, camera_frame_setup, camera_rays_setup
+    from paper_2504_18001_b200.sampler import point_to_unit_box
+    from scene_specs import SESSION_SPECS
+
+    rng = np.random.default_rng(3)
+    n = 0
+    for i in range(3000):
+        up = (0.0, 1.0, 0.0) if i % 2 else tuple(rng.normal(0.0, 1.0, 3))
+        try:
+            cam = Camera(tuple(rng.normal(0.5, 2.0, 3)), tuple(rng.random(3)), up, float(rng.uniform(5.0, 150.0)),
+                         int(rng.integers(8, 4096)), int(rng.integers(8, 4096)))
+        except ConfigError:
+            continue
+        rot, th, tv = camera_rays_setup(cam)
+        o, r9, th2, tv2, d = camera_frame_setup(cam)
+        np.testing.assert_array_equal(np.array(r9), rot.ravel())
+        assert (th2, tv2) == (th, tv) and o == tuple(float(x) for x in cam.position)
+        assert d == point_to_unit_box(np.asarray(cam.position, dtype=np.float64))
+        n += 1
+    assert n > 2500
+    ops = load_golden("ops_lattice64.npz")
+    spec = SESSION_SPECS["lattice64"]
+    cam = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=96, height=96).camera_at(spec["op_frame"] * spec["cam_step"])
+    o, r9, th, tv, _ = camera_frame_setup(cam)
+    np.testing.assert_array_equal(np.array(r9).reshape(3, 3), ops["raygen0_in1"])
+    assert th == float(ops["raygen0_in3"]) and tv == float(ops["raygen0_in4"])
+
+
 def test_inr_init_sequence_vs_reference():
     import hashlib
 
