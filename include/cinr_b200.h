@@ -351,6 +351,15 @@ int32_t vcb_maintenance(const VcbMaintParams *p, void *stream);
  * defer_decode = 1 selected, on `stream`: the caller orders it after that maintenance
  * and before the next one (events), so it overlaps the next frame's march. */
 int32_t vcb_maint_decode(const VcbMaintParams *p, void *stream);
+/* The maintenance as one CUDA graph (north_star subsystem 4: the per-frame launch
+ * sequence captured once, replayed per frame).  vcb_maint_graph_create captures
+ * vcb_maintenance's launches for `p`; every field but session_frame must stay the same
+ * for the graph's life (the caller keys the graph on them).  vcb_maint_graph_launch
+ * sets session_frame in the captured kernels and launches the graph on `stream`: the
+ * results are vcb_maintenance's. */
+int32_t vcb_maint_graph_create(const VcbMaintParams *p, void **graph);
+int32_t vcb_maint_graph_launch(void *graph, const VcbMaintParams *p, void *stream);
+void vcb_maint_graph_destroy(void *graph);
 
 #ifdef __cplusplus
 }

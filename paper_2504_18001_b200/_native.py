@@ -146,6 +146,9 @@ _PROTOS = {
     "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
     "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
     "vcb_maint_decode": (i32, [C.POINTER(VcbMaintParams), vp]),
+    "vcb_maint_graph_create": (i32, [C.POINTER(VcbMaintParams), C.POINTER(vp)]),
+    "vcb_maint_graph_launch": (i32, [vp, C.POINTER(VcbMaintParams), vp]),
+    "vcb_maint_graph_destroy": (None, [vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

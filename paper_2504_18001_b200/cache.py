@@ -230,6 +230,7 @@ class DeviceCache:
         self.staged_keys = t(mr, torch.int64, -1)
         wsb = N.load().vcb_maint_workspace_bytes(lay.total, self.slots, mr)
         self.workspace = torch.zeros(wsb, dtype=torch.uint8, device=device)
+        self._graph, self._graph_key = None, None  # the maintenance CUDA graph (maintenance(graph=True))
         self.dbg_reports = t(2 * lay.total, torch.int64, 0) if debug else None
         # the request table's keys as a compacted list (k_pending reads it instead of
         # scanning every brick's req_base: 19.4 M bricks at 4096^3@B16); list_counts[1]
@@ -286,13 +287,38 @@ class DeviceCache:
         p.defer_decode = 1 if defer_decode else 0
         return p
 
-    def maintenance(self, session_frame: int, field_desc, stream=None, frame_stats=None, defer_decode=False):
+    def maintenance(self, session_frame: int, field_desc, stream=None, frame_stats=None, defer_decode=False,
+                    graph=False):
         """vcb_maintenance.  frame_stats = device address of the frame's VcbFrameStats (a
         failed frame then skips the maintenance on the device; the decode budget's share
-        the frame used).  defer_decode: the batch is left for decode() on another stream."""
+        the frame used).  defer_decode: the batch is left for decode() on another stream.
+        graph: replay the maintenance as one CUDA graph (vcb_maint_graph_*), captured
+        again whenever a parameter other than the session frame changes."""
         p = self.maint_params(session_frame, field_desc, frame_stats, defer_decode)
         self._last_params = p
-        N.call("vcb_maintenance", C.byref(p), stream_ptr(stream))
+        if not graph:
+            N.call("vcb_maintenance", C.byref(p), stream_ptr(stream))
+            return
+        q = N.VcbMaintParams.from_buffer_copy(p)
+        q.session_frame = 0
+        key = bytes(q)
+        if self._graph is None or self._graph_key != key:
+            self.drop_graph()
+            h = C.c_void_p()
+            N.call("vcb_maint_graph_create", C.byref(p), C.byref(h))
+            self._graph, self._graph_key = h, key
+        N.call("vcb_maint_graph_launch", self._graph, C.byref(p), stream_ptr(stream))
+
+    def drop_graph(self):
+        if getattr(self, "_graph", None) is not None:
+            N.load().vcb_maint_graph_destroy(self._graph)
+        self._graph, self._graph_key = None, None
+
+    def __del__(self):
+        try:
+            self.drop_graph()
+        except Exception:
+            pass
 
     def decode(self, stream):
         """The deferred fulfill of the batch the last maintenance selected (vcb_maint_decode)."""

@@ -15,6 +15,7 @@
 //   field decode  fulfill (scheduler.py:127-134) into the staging slab; a
 //                 non-finite decode re-enters the keys with base=f (164-168)
 #include <cstddef>
+#include <vector>
 
 #include "common.cuh"
 #include "fields.cuh"
@@ -587,9 +588,7 @@ static void maint_decode(const VcbMaintParams& P, const MaintWs& w, cudaStream_t
     k_post_decode<<<1, 1, 0, st>>>(P, w);
 }
 
-extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
-    const VcbMaintParams& P = *pp;
-    cudaStream_t st = (cudaStream_t)stream_;
+static int32_t maint_enqueue(const VcbMaintParams& P, cudaStream_t st) {
     if (P.max_requests < 1) return set_error("maintenance: batch size must be >= 1");
     if (P.max_requests > kMaxSel) return set_error("maintenance: max_requests > %d unsupported", kMaxSel);
     MaintWs w;
@@ -612,6 +611,105 @@ extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
     if (!P.defer_decode) maint_decode(P, w, st);
     g_launches += P.defer_decode ? 5 : 7;
     return check_launch("maintenance");
+}
+
+extern "C" int32_t vcb_maintenance(const VcbMaintParams* pp, void* stream_) {
+    return maint_enqueue(*pp, (cudaStream_t)stream_);
+}
+
+// The maintenance as one CUDA graph: captured once per static configuration, then
+// replayed each frame with session_frame updated in the kernels that take the
+// maintenance parameters (the decode's arguments do not depend on the frame).
+struct MaintGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaGraphNode_t> nodes;
+    std::vector<cudaKernelNodeParams> kp;
+    MaintWs w;
+    long long launches = 0;
+};
+
+static bool takes_maint_params(const void* fn) {
+    return fn == (const void*)k_maint_gate || fn == (const void*)k_report || fn == (const void*)k_insert ||
+           fn == (const void*)k_pending || fn == (const void*)k_select || fn == (const void*)k_post_decode;
+}
+
+static void maint_graph_free(MaintGraph* g) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+}
+
+extern "C" int32_t vcb_maint_graph_create(const VcbMaintParams* pp, void** out) {
+    *out = nullptr;
+    const VcbMaintParams& P = *pp;
+    MaintGraph* g = new MaintGraph();
+    if (maint_ws_layout(P.total, P.workspace, &g->w) > P.workspace_bytes) {
+        delete g;
+        return set_error("maint_graph: workspace too small");
+    }
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+        delete g;
+        return check_launch("maint_graph stream");
+    }
+    const long long before = g_launches;
+    cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    const int32_t rc = maint_enqueue(P, cs);
+    const cudaError_t e = cudaStreamEndCapture(cs, &g->graph);
+    cudaStreamDestroy(cs);
+    g->launches = g_launches - before;
+    g_launches = before;
+    if (rc != 0 || e != cudaSuccess) {
+        maint_graph_free(g);
+        return rc != 0 ? rc : set_error("maint_graph: capture failed: %s", cudaGetErrorString(e));
+    }
+    size_t n = 0;
+    cudaGraphGetNodes(g->graph, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    cudaGraphGetNodes(g->graph, nodes.data(), &n);
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        cudaGraphKernelNodeGetParams(nd, &kp);
+        if (!takes_maint_params(kp.func)) continue;
+        g->nodes.push_back(nd);
+        g->kp.push_back(kp);
+    }
+    const size_t want = P.defer_decode ? 5 : 6;
+    if (g->nodes.size() != want) {
+        maint_graph_free(g);
+        return set_error("maint_graph: %zu parameterised kernels captured, expected %zu", g->nodes.size(), want);
+    }
+    if (cudaGraphInstantiate(&g->exec, g->graph, 0) != cudaSuccess) {
+        maint_graph_free(g);
+        return check_launch("maint_graph instantiate");
+    }
+    *out = g;
+    return 0;
+}
+
+extern "C" int32_t vcb_maint_graph_launch(void* handle, const VcbMaintParams* pp, void* stream_) {
+    MaintGraph* g = (MaintGraph*)handle;
+    if (!g) return set_error("maint_graph: null graph");
+    VcbMaintParams P = *pp;  // kernel arguments are copied by SetParams
+    void* args[2] = {&P, &g->w};
+    for (size_t i = 0; i < g->nodes.size(); i++) {
+        cudaKernelNodeParams kp = g->kp[i];
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        if (cudaGraphExecKernelNodeSetParams(g->exec, g->nodes[i], &kp) != cudaSuccess)
+            return check_launch("maint_graph set params");
+    }
+    cudaGraphLaunch(g->exec, (cudaStream_t)stream_);
+    g_launches += g->launches;
+    return check_launch("maint_graph launch");
+}
+
+extern "C" void vcb_maint_graph_destroy(void* handle) {
+    if (handle) maint_graph_free((MaintGraph*)handle);
 }
 
 extern "C" int32_t vcb_maint_decode(const VcbMaintParams* pp, void* stream_) {

@@ -118,6 +118,7 @@ class RenderSession:
         self.impl = 0  # march schedule (VcbFrameParams.impl), set through `march`
         self.march = march
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
+        self.maint_graph = True  # replay the maintenance as one CUDA graph (False: kernel by kernel)
         self._target = None  # whole-frame buffer written in place (fused sort-first gather)
         self._pin_free = []  # pinned host frames released by callers
         # loader="thread" (the reference's default, a background decode thread): the batch a
@@ -413,7 +414,7 @@ class RenderSession:
                 if self._ev_decoded is not None:
                     self.stream.wait_event(self._ev_decoded)  # the batch this maintenance inserts
                 self.cache.maintenance(self.frame, self._dfield.desc, self.stream, frame_stats=ptr(self._stats),
-                                       defer_decode=self._dstream is not None)
+                                       defer_decode=self._dstream is not None, graph=self.maint_graph)
                 if self._dstream is not None:
                     sel = torch.cuda.Event()
                     sel.record(self.stream)

@@ -51,8 +51,8 @@ def macro_from(dims, vmin, vmax, cell=16):
                                    np.ones_like(vmin, dtype=np.float32))
 
 
-def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0):
-    """Yields (frame, img, record, session)."""
+def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0, maint_graph=None):
+    """Yields (frame, img, record, session).  maint_graph: None = the session default."""
     from paper_2504_18001_b200.harness import OrbitTrajectory
     from paper_2504_18001_b200.session import RenderSession
 
@@ -62,6 +62,8 @@ def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0):
     mg = macro_from(spec["dims"], *macro) if macro is not None else None
     sess = RenderSession(fld, product_tf(spec["tf"]), traj.camera_at(0), product_config(spec), macro=mg, debug=debug)
     sess.impl = impl
+    if maint_graph is not None:
+        sess.maint_graph = maint_graph
     events = spec.get("events", {})
     for f in range(frames if frames is not None else spec["frames"]):
         ev = events.get(f)

@@ -90,6 +90,21 @@ def test_session_bit_exact_vs_reference(name):
         assert diff <= 1e-6, f"frame {f} image max abs diff {diff}"
 
 
+@pytest.mark.parametrize("name", ["pressure", "events", "lattice64_fifo"])
+def test_maintenance_launch_modes_bit_exact_vs_reference(name):
+    """The maintenance replayed as one CUDA graph and launched kernel by kernel (the
+    mode the session does not use by default) give the reference's state every frame
+    (eviction, deferral, TF switch + reset events, FIFO)."""
+    from gpu_runner import run_gpu_session
+    g = load_golden(f"session_{name}.npz")
+    for graph in (True, False):
+        for f, img, rec, sess in run_gpu_session(name, macro=(g["macro_vmin"], g["macro_vmax"]), maint_graph=graph):
+            st = sess.debug_state()
+            for k in ("tables", "owner", "last_used", "entries", "reports", "batch"):
+                np.testing.assert_array_equal(st[k], g[f"f{f}_{k}"], err_msg=f"graph={graph} frame {f} {k}")
+            assert np.abs(img - g[f"f{f}_img"]).max() <= 1e-6, f"graph={graph} frame {f}"
+
+
 @pytest.mark.parametrize("name", ["inr64", "inr_uncached", "pt_inr", "pt_inr_uncached"])
 def test_session_inr_vs_reference(name):
     """Random-init hash-grid INR: images within 1e-3 abs (>= 60 dB), cache state bit-exact."""

@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import bench  # noqa: E402
 
 
-def main(preroll=60, n=50):
+def main(preroll=60, n=50, graph=False):
     import paper_2504_18001_b200 as P
     from paper_2504_18001_b200 import macrocell
     from paper_2504_18001_b200.harness import OrbitTrajectory
@@ -23,6 +23,7 @@ def main(preroll=60, n=50):
     cfg = bench.session_config(P, SessionConfig)
     traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=1024, height=1024)
     s = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, march="throughput")
+    s.maint_graph = graph
     for f in range(preroll):
         s.set_camera(traj.camera_at(f))
         s.render_frame_device()
@@ -46,9 +47,10 @@ def main(preroll=60, n=50):
         post.append(s._ev_t1.elapsed_time(e1) * 1e3)
         host.append((h1 - h0) * 1e6)
     med = statistics.median
-    print(f"prologue {med(pro):.1f} us, frame kernels {med(mar):.1f} us, after {med(post):.1f} us, "
+    print(f"maint_graph={graph}: prologue {med(pro):.1f} us, frame kernels {med(mar):.1f} us, after {med(post):.1f} us, "
           f"host submit {med(host):.1f} us")
 
 
 if __name__ == "__main__":
-    main()
+    for g in (False, True, False, True):
+        main(graph=g)
