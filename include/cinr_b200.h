@@ -164,9 +164,10 @@ typedef struct {
                                 wavefront iteration, sampler.py:206-213): 0 = one-barrier persistent
                                 wavefront, 384 threads/CTA (default), 9 = the same at 512 threads,
                                 1 = one launch per iteration (cross-check).  Throughput (RNG lane = film
-                                pixel, no grid barrier): 10/11/12 = one persistent ray per lane at
-                                512/768/1024 threads/CTA.  Path tracing: 1 = four-barrier walk,
-                                otherwise the default walk */
+                                pixel, no grid barrier, one persistent ray per lane): 10 = 512 threads/CTA,
+                                skip budget 2 (default); 11 = 512, 1; 12 = 640, 1; 13 = 512, unbounded;
+                                14 = 640, 2.  Path tracing: 1 = four-barrier walk, otherwise the default
+                                walk */
     int32_t image_global;    /* 0: image is this session's band [rows][W][4]; 1: image is the whole
                                 frame [height][W][4] (possibly a peer GPU's buffer mapped over NVLink)
                                 and local row j lands on film row row0 + j*row_step */

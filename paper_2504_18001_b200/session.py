@@ -375,12 +375,18 @@ class RenderSession:
         rng.bit_generator.advance(int(draws[0]))
         return t_hit.cpu().numpy(), v_hit.cpu().numpy()
 
-    def render_frame_device(self):
+    def render_frame_device(self, out=None):
         """Render + maintenance on the session stream; returns the device image
-        (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame."""
+        (H, W, 4) f32 without synchronising.  `collect_record()` finishes the frame.
+        out: a (rows, W, 4) f32 buffer the frame kernels write instead (render_frame
+        passes a pinned host frame: the pixels cross PCIe as the rays retire)."""
         W, H = int(self.camera.width), int(self.camera.height)
         R = self._band_rows(H)
-        if self._target is not None:
+        if out is not None:
+            if tuple(out.shape) != (R, W, 4) or out.dtype != torch.float32:
+                raise ValueError(f"frame buffer {tuple(out.shape)} {out.dtype} != {(R, W, 4)} float32")
+            img = out
+        elif self._target is not None:
             if tuple(self._target.shape) != (H, W, 4):
                 raise ValueError(f"frame target shape {tuple(self._target.shape)} != {(H, W, 4)}")
             img = self._target
@@ -450,8 +456,17 @@ class RenderSession:
         return rec
 
     def render_frame(self):
-        """Render, then run the maintenance phase; returns (image f32[H,W,4] on host, FrameRecord)."""
+        """Render, then run the maintenance phase; returns (image f32[H,W,4] on host, FrameRecord).
+        The frame kernels store the pixels straight into a pinned host frame (mapped
+        memory), so the image transfer overlaps the march instead of following it."""
         t0 = time.perf_counter()
+        if self._target is None:
+            host = self._pinned((self._band_rows(int(self.camera.height)), int(self.camera.width), 4))
+            self.render_frame_device(out=host)
+            rec = self.collect_record(t0)
+            out = host.numpy()
+            weakref.finalize(out, self._pin_free.append, host)
+            return out, rec
         img = self.render_frame_device()
         host = self._pinned(tuple(img.shape))
         # the copy waits only for the frame kernel, not for the maintenance after it
