@@ -358,6 +358,26 @@ int32_t vcb_maint_decode(const VcbMaintParams *p, void *stream);
  * for the graph's life (the caller keys the graph on them).  vcb_maint_graph_launch
  * sets session_frame in the captured kernels and launches the graph on `stream`: the
  * results are vcb_maintenance's. */
+/* Brick-decode sharing across ranks (SURVEY §8e "optional brick sharing"; the
+ * collectives are the caller's).  vcb_share_keys writes [n, staged keys...] of the last
+ * maintenance (max_requests + 1 int64).  With those rows of all `world` ranks,
+ * vcb_share_plan lists the distinct keys this rank owns (owner = splitmix64(key) % world;
+ * up to `cap`, in key order: counts[0]), where each of its own batch keys sits in the
+ * gathered slabs (src[i] = owner * cap + slot, -1 = decode locally) and the keys to
+ * decode locally (ovf_keys / ovf_idx, counts[1]).  vcb_share_decode decodes a device-
+ * counted key list (the owned keys, the local ones); vcb_share_scatter fills the staging
+ * slab from the gathered slabs and the local bricks, merges the owners' decode-failure
+ * flags and runs the failure path (scheduler.py:164-168) — the state equals the
+ * unshared maintenance's. */
+int32_t vcb_share_keys(const VcbMaintParams *p, int64_t *out, void *stream);
+int32_t vcb_share_plan(const int64_t *all_keys, int32_t world, int32_t rank, int32_t max_requests, int32_t cap,
+                       int64_t *own_keys, int64_t *counts, int32_t *src, int64_t *ovf_keys, int32_t *ovf_idx,
+                       void *stream);
+int32_t vcb_share_decode(const VcbMaintParams *p, const int64_t *keys, const int64_t *n_keys, int32_t max_keys,
+                         float *out, int32_t *nonfinite, void *stream);
+int32_t vcb_share_scatter(const VcbMaintParams *p, const float *gathered, const int32_t *flags, int32_t cap,
+                          const int32_t *src, const float *ovf_out, const int32_t *ovf_idx, const int64_t *counts,
+                          const int32_t *ovf_flag, void *stream);
 int32_t vcb_maint_graph_create(const VcbMaintParams *p, void **graph);
 int32_t vcb_maint_graph_launch(void *graph, const VcbMaintParams *p, void *stream);
 void vcb_maint_graph_destroy(void *graph);

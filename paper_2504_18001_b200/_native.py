@@ -146,6 +146,10 @@ _PROTOS = {
     "vcb_maint_workspace_bytes": (i64, [i64, i64, i32]),
     "vcb_maintenance": (i32, [C.POINTER(VcbMaintParams), vp]),
     "vcb_maint_decode": (i32, [C.POINTER(VcbMaintParams), vp]),
+    "vcb_share_keys": (i32, [C.POINTER(VcbMaintParams), vp, vp]),
+    "vcb_share_plan": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "vcb_share_decode": (i32, [C.POINTER(VcbMaintParams), vp, vp, i32, vp, vp, vp]),
+    "vcb_share_scatter": (i32, [C.POINTER(VcbMaintParams), vp, vp, i32, vp, vp, vp, vp, vp, vp]),
     "vcb_maint_graph_create": (i32, [C.POINTER(VcbMaintParams), C.POINTER(vp)]),
     "vcb_maint_graph_launch": (i32, [vp, C.POINTER(VcbMaintParams), vp]),
     "vcb_maint_graph_destroy": (None, [vp]),

@@ -573,19 +573,128 @@ extern "C" int64_t vcb_maint_workspace_bytes(int64_t total_bricks, int64_t slots
 
 // fulfill (scheduler.py:127-134) of the batch k_select staged (w.n_dec keys, 0 when the
 // maintenance was skipped) into the staging slab, then the failure path (k_post_decode)
-static void maint_decode(const VcbMaintParams& P, const MaintWs& w, cudaStream_t st) {
+// Decode bricks `keys` (count on the device) of P's field into `out` ([max_keys][B^3]).
+static void decode_keys(const VcbMaintParams& P, const int64_t* keys, const int64_t* n_dev, int max_keys, float* out,
+                        int32_t* nonfinite, cudaStream_t st) {
     const int sm = mlp_smem_bytes(P.field);
     const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
-    const int gdec = grid_for((int64_t)P.max_requests * b3, 128, 8);
-    const int64_t* nst = (const int64_t*)w.n_dec();
+    const int gdec = grid_for((int64_t)max_keys * b3, 128, 8);
     if (P.field.kind == 0 && inr_is_default(P.field)) {
         // the default INR decodes on the tensor cores (tcgen05, decode_tc.cu)
-        inr_bricks_tc_dev(P.field, P.geom, P.staged_keys, nst, P.max_requests, P.staging, w.nonfinite, st);
+        inr_bricks_tc_dev(P.field, P.geom, keys, n_dev, max_keys, out, nonfinite, st);
     } else {
-        CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, P.staged_keys, nst,
-                          P.max_requests, P.staging, w.nonfinite);
+        CINR_DISPATCH_INR(P.field, k_decode_bricks_dev, gdec, 128, sm, st, P.field, P.geom, keys, n_dev, max_keys, out,
+                          nonfinite);
     }
+}
+
+static void maint_decode(const VcbMaintParams& P, const MaintWs& w, cudaStream_t st) {
+    decode_keys(P, P.staged_keys, (const int64_t*)w.n_dec(), P.max_requests, P.staging, w.nonfinite, st);
     k_post_decode<<<1, 1, 0, st>>>(P, w);
+}
+
+// ---- brick-decode sharing across ranks (SURVEY §8e "optional brick sharing"): every
+// rank's batch keys are all-gathered; each unique key is decoded once, by its owner
+// rank (splitmix64(key) % world), into that owner's slab; the slabs are all-gathered
+// and each rank copies its batch's bricks into its staging slab.  A key an owner cannot
+// fit (more than `cap` owned keys) is decoded by every rank that needs it.  The decoder
+// is deterministic per key, so staging equals the unshared decode bit for bit.
+__device__ __forceinline__ int share_owner(long long key, int world) {
+    return (int)(splitmix64((u64)key) % (u64)world);
+}
+
+// [n_dec, staged_keys[0..mr)] of this maintenance (n_dec = 0 when it was skipped)
+__global__ void k_share_keys(VcbMaintParams P, MaintWs w, long long* out) {
+    const long long n = *w.n_dec();
+    for (int i = threadIdx.x; i <= P.max_requests; i += blockDim.x)
+        out[i] = i == 0 ? n : (i - 1 < n ? P.staged_keys[i - 1] : -1);
+}
+
+// One CTA.  all: world rows of `stride` = mr + 1 ([n, keys...]).  Quadratic in the
+// gathered keys (world * mr): a few hundred at the default batch.
+__global__ void __launch_bounds__(1024) k_share_plan(const long long* all, int world, int rank, int stride, int cap,
+                                                     long long* own, long long* counts, int32_t* src,
+                                                     long long* ovf_keys, int32_t* ovf_idx) {
+    extern __shared__ long long sk[];  // [M] keys (-1: none), then [M] owner of a first occurrence (-1: none)
+    const int mr = stride - 1, M = world * mr;
+    int* so = reinterpret_cast<int*>(sk + M);
+    __shared__ int n_own, n_ovf;
+    if (threadIdx.x == 0) n_own = n_ovf = 0;
+    for (int t = threadIdx.x; t < M; t += blockDim.x) {
+        const int q = t / mr, i = t - q * mr;
+        sk[t] = i < all[(long long)q * stride] ? all[(long long)q * stride + 1 + i] : -1;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < M; t += blockDim.x) {
+        const long long k = sk[t];
+        bool first = k >= 0;
+        for (int u = 0; u < t && first; u++) first = sk[u] != k;
+        so[t] = first ? share_owner(k, world) : -1;
+    }
+    __syncthreads();
+    // slot of a key = its rank among the distinct keys its owner holds
+    auto slot_of = [&](long long k, int o) {
+        int s = 0;
+        for (int u = 0; u < M; u++) s += (so[u] == o && sk[u] < k);
+        return s;
+    };
+    for (int t = threadIdx.x; t < M; t += blockDim.x) {
+        const long long k = sk[t];
+        if (so[t] != rank) continue;
+        const int s = slot_of(k, rank);
+        if (s < cap) {
+            own[s] = k;
+            atomicAdd(&n_own, 1);
+        }
+    }
+    const long long n_mine = all[(long long)rank * stride];
+    for (int i = threadIdx.x; i < mr; i += blockDim.x) {
+        if (i >= n_mine) {
+            src[i] = -1;
+            continue;
+        }
+        const long long k = sk[rank * mr + i];
+        const int o = share_owner(k, world);
+        const int s = slot_of(k, o);
+        if (s < cap) {
+            src[i] = o * cap + s;
+        } else {
+            src[i] = -1;
+            const int j = atomicAdd(&n_ovf, 1);
+            ovf_keys[j] = k;
+            ovf_idx[j] = i;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        counts[0] = n_own;
+        counts[1] = n_ovf;
+    }
+}
+
+// staging[i] <- gathered slab brick src[i] (or the locally decoded overflow brick);
+// the decode-failure flag of the bricks this rank uses feeds k_post_decode
+__global__ void k_share_scatter(VcbMaintParams P, MaintWs w, const float* gathered, const int32_t* flags, int cap,
+                                const int32_t* src, const float* ovf_out, const int32_t* ovf_idx,
+                                const long long* counts, const int32_t* ovf_flag) {
+    const long long b3 = P.geom.b * P.geom.b * P.geom.b;
+    const long long n = *w.n_dec(), n_ovf = counts[1];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n * b3; t += stride) {
+        const long long i = t / b3, e = t - i * b3;
+        const int s = src[i];
+        if (s >= 0) P.staging[t] = gathered[(long long)s * b3 + e];
+    }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_ovf * b3; t += stride) {
+        const long long j = t / b3, e = t - j * b3;
+        P.staging[(long long)ovf_idx[j] * b3 + e] = ovf_out[t];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int bad = n_ovf > 0 && *ovf_flag != 0;
+        for (long long i = 0; i < n && !bad; i++)
+            if (src[i] >= 0 && flags[src[i] / cap]) bad = 1;
+        if (bad) w.nonfinite[0] = 1;
+    }
 }
 
 static int32_t maint_enqueue(const VcbMaintParams& P, cudaStream_t st) {
@@ -710,6 +819,50 @@ extern "C" int32_t vcb_maint_graph_launch(void* handle, const VcbMaintParams* pp
 
 extern "C" void vcb_maint_graph_destroy(void* handle) {
     if (handle) maint_graph_free((MaintGraph*)handle);
+}
+
+extern "C" int32_t vcb_share_keys(const VcbMaintParams* pp, int64_t* out, void* stream_) {
+    const VcbMaintParams& P = *pp;
+    MaintWs w;
+    if (maint_ws_layout(P.total, P.workspace, &w) > P.workspace_bytes) return set_error("share_keys: workspace");
+    k_share_keys<<<1, 256, 0, (cudaStream_t)stream_>>>(P, w, (long long*)out);
+    return check_launch("share_keys");
+}
+
+extern "C" int32_t vcb_share_plan(const int64_t* all_keys, int32_t world, int32_t rank, int32_t max_requests,
+                                  int32_t cap, int64_t* own_keys, int64_t* counts, int32_t* src, int64_t* ovf_keys,
+                                  int32_t* ovf_idx, void* stream_) {
+    const int M = world * max_requests;
+    const size_t smem = (size_t)M * 12;
+    if (world < 1 || rank < 0 || rank >= world || max_requests < 1 || cap < 1 || smem > 200 * 1024)
+        return set_error("share_plan: world %d rank %d batch %d cap %d", world, rank, max_requests, cap);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_share_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_share_plan<<<1, 1024, smem, (cudaStream_t)stream_>>>((const long long*)all_keys, world, rank, max_requests + 1,
+                                                            cap, (long long*)own_keys, (long long*)counts, src,
+                                                            (long long*)ovf_keys, ovf_idx);
+    return check_launch("share_plan");
+}
+
+extern "C" int32_t vcb_share_decode(const VcbMaintParams* pp, const int64_t* keys, const int64_t* n_keys,
+                                    int32_t max_keys, float* out, int32_t* nonfinite, void* stream_) {
+    decode_keys(*pp, keys, n_keys, max_keys, out, nonfinite, (cudaStream_t)stream_);
+    g_launches += 1;
+    return check_launch("share_decode");
+}
+
+extern "C" int32_t vcb_share_scatter(const VcbMaintParams* pp, const float* gathered, const int32_t* flags,
+                                     int32_t cap, const int32_t* src, const float* ovf_out, const int32_t* ovf_idx,
+                                     const int64_t* counts, const int32_t* ovf_flag, void* stream_) {
+    const VcbMaintParams& P = *pp;
+    MaintWs w;
+    if (maint_ws_layout(P.total, P.workspace, &w) > P.workspace_bytes) return set_error("share_scatter: workspace");
+    cudaStream_t st = (cudaStream_t)stream_;
+    const int64_t b3 = P.geom.b * P.geom.b * P.geom.b;
+    k_share_scatter<<<grid_for((int64_t)P.max_requests * b3, 256, 4), 256, 0, st>>>(
+        P, w, gathered, flags, cap, src, ovf_out, ovf_idx, (const long long*)counts, ovf_flag);
+    k_post_decode<<<1, 1, 0, st>>>(P, w);
+    g_launches += 2;
+    return check_launch("share_scatter");
 }
 
 extern "C" int32_t vcb_maint_decode(const VcbMaintParams* pp, void* stream_) {

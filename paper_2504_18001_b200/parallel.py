@@ -234,6 +234,74 @@ class FrameGather:
         self.drain()
 
 
+class BrickShare:
+    """Brick-decode sharing across ranks (SURVEY §8e "optional brick sharing").
+
+    Every rank's maintenance selects its own batch for its private cache.  The batches'
+    keys are all-gathered; each distinct key is decoded once, by its owner rank
+    (splitmix64(key) % world), into a fixed slab of `cap` bricks; the slabs are
+    all-gathered and each rank fills its staging slab from them (vcb_share_*).  With
+    sort-first bands the ranks' batches overlap, so a rank decodes about 1/world of
+    what it would alone; the cache state is unchanged (the decoder is deterministic
+    per key).  NCCL all-gathers on the session stream; gloo (ranks sharing a GPU in the
+    functional checks) goes through host memory."""
+
+    def __init__(self, ctx: Ctx, sess):
+        c = sess.cache
+        if c is None:
+            raise ValueError("brick sharing needs a cached session")
+        self.ctx, self.sess = ctx, sess
+        dev = sess.device
+        mr = int(c.sched.max_requests)
+        b3 = int(c.geom.b) ** 3
+        W = ctx.world
+        self.mr, self.cap, self.b3 = mr, mr, b3
+        e = lambda n, dt: torch.empty(n, dtype=dt, device=dev)
+        self.keys = e(mr + 1, torch.int64)
+        self.keys_all = e(W * (mr + 1), torch.int64)
+        self.own, self.counts = e(self.cap, torch.int64), torch.zeros(2, dtype=torch.int64, device=dev)
+        self.src, self.ovf_keys, self.ovf_idx = e(mr, torch.int32), e(mr, torch.int64), e(mr, torch.int32)
+        self.slab, self.flag = e(self.cap * b3, torch.float32), torch.zeros(1, dtype=torch.int32, device=dev)
+        self.gathered, self.flags = e(W * self.cap * b3, torch.float32), e(W, torch.int32)
+        self.ovf_out, self.ovf_flag = e(mr * b3, torch.float32), torch.zeros(1, dtype=torch.int32, device=dev)
+        self.decoded = 0  # bricks this rank decoded (owned + local), host-side count for reports
+
+    def _all_gather(self, out, inp):
+        if self.ctx.world == 1:
+            out.copy_(inp)
+        elif self.ctx.backend == "nccl":
+            dist.all_gather_into_tensor(out, inp)
+        else:
+            torch.cuda.current_stream().synchronize()
+            h = inp.cpu()
+            parts = [torch.empty_like(h) for _ in range(self.ctx.world)]
+            dist.all_gather(parts, h)
+            out.copy_(torch.cat(parts))
+
+    def run(self, params, stream):
+        """After a maintenance with defer_decode=1 (params: its VcbMaintParams)."""
+        import ctypes as C
+
+        from . import _native as N
+        from .device import ptr, stream_ptr
+
+        sp, pp = stream_ptr(stream), C.byref(params)
+        with torch.cuda.stream(stream):
+            N.call("vcb_share_keys", pp, ptr(self.keys), sp)
+            self._all_gather(self.keys_all, self.keys)
+            N.call("vcb_share_plan", ptr(self.keys_all), self.ctx.world, self.ctx.rank, self.mr, self.cap,
+                   ptr(self.own), ptr(self.counts), ptr(self.src), ptr(self.ovf_keys), ptr(self.ovf_idx), sp)
+            self.flag.zero_()
+            N.call("vcb_share_decode", pp, ptr(self.own), ptr(self.counts), self.cap, ptr(self.slab), ptr(self.flag), sp)
+            self._all_gather(self.gathered, self.slab)
+            self._all_gather(self.flags, self.flag)
+            self.ovf_flag.zero_()
+            N.call("vcb_share_decode", pp, ptr(self.ovf_keys), ptr(self.counts[1:]), self.mr, ptr(self.ovf_out),
+                   ptr(self.ovf_flag), sp)
+            N.call("vcb_share_scatter", pp, ptr(self.gathered), ptr(self.flags), self.cap, ptr(self.src),
+                   ptr(self.ovf_out), ptr(self.ovf_idx), ptr(self.counts), ptr(self.ovf_flag), sp)
+
+
 def barrier(ctx: Ctx):
     if ctx.world > 1:
         dist.barrier()

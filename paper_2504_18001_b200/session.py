@@ -119,6 +119,7 @@ class RenderSession:
         self.march = march
         self.band = (0, 1)  # film rows row0, row0+step, ... (sort-first multi-GPU)
         self.maint_graph = True  # replay the maintenance as one CUDA graph (False: kernel by kernel)
+        self._share = None  # parallel.BrickShare: brick decodes shared across ranks (share_decode)
         self._target = None  # whole-frame buffer written in place (fused sort-first gather)
         self._pin_free = []  # pinned host frames released by callers
         # loader="thread" (the reference's default, a background decode thread): the batch a
@@ -152,6 +153,16 @@ class RenderSession:
         if name not in self.MARCH_SCHEDULES:
             raise ValueError(f"unknown march schedule {name!r} (parity | throughput)")
         self.impl = self.MARCH_SCHEDULES[name]
+
+    def share_decode(self, ctx):
+        """Decode each frame's brick batch jointly with the other ranks of `ctx`
+        (parallel.BrickShare): every distinct requested brick is decoded once, by its
+        owner rank, and all-gathered.  Same cache state as decoding alone; with
+        loader="thread" the decode then runs on the session stream.  ctx=None turns it off."""
+        from .parallel import BrickShare
+
+        self._sync_decode()
+        self._share = BrickShare(ctx, self) if ctx is not None else None
 
     def set_band(self, row0: int, row_step: int):
         """Render only film rows row0 + j*row_step (one rank's share of a frame)."""
@@ -420,8 +431,11 @@ class RenderSession:
                 if self._ev_decoded is not None:
                     self.stream.wait_event(self._ev_decoded)  # the batch this maintenance inserts
                 self.cache.maintenance(self.frame, self._dfield.desc, self.stream, frame_stats=ptr(self._stats),
-                                       defer_decode=self._dstream is not None, graph=self.maint_graph)
-                if self._dstream is not None:
+                                       defer_decode=self._dstream is not None or self._share is not None,
+                                       graph=self.maint_graph)
+                if self._share is not None:
+                    self._share.run(self.cache._last_params, self.stream)
+                elif self._dstream is not None:
                     sel = torch.cuda.Event()
                     sel.record(self.stream)
                     self._dstream.wait_event(sel)

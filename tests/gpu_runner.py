@@ -51,8 +51,9 @@ def macro_from(dims, vmin, vmax, cell=16):
                                    np.ones_like(vmin, dtype=np.float32))
 
 
-def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0, maint_graph=None):
-    """Yields (frame, img, record, session).  maint_graph: None = the session default."""
+def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0, maint_graph=None, setup=None):
+    """Yields (frame, img, record, session).  maint_graph: None = the session default;
+    setup(session) runs before the first frame."""
     from paper_2504_18001_b200.harness import OrbitTrajectory
     from paper_2504_18001_b200.session import RenderSession
 
@@ -64,6 +65,8 @@ def run_gpu_session(name, macro=None, frames=None, debug=True, impl=0, maint_gra
     sess.impl = impl
     if maint_graph is not None:
         sess.maint_graph = maint_graph
+    if setup is not None:
+        setup(sess)
     events = spec.get("events", {})
     for f in range(frames if frames is not None else spec["frames"]):
         ev = events.get(f)
