@@ -390,6 +390,9 @@ def main():
     ap.add_argument("--mp", default="tiles", choices=["tiles", "frames"],
                     help="N>1: 'tiles' = sort-first film-row bands of every frame, RGBA8 bands gathered to rank 0 "
                          "(strong scaling, default); 'frames' = alternate-frame rendering (weak scaling)")
+    ap.add_argument("--share-decode", action="store_true",
+                    help="N>1: decode each distinct requested brick once, on its owner rank, and all-gather "
+                         "(RenderSession.share_decode; the cache state is unchanged)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -431,6 +434,8 @@ def main():
     sess.march = args.march
     if args.schedule is not None:
         sess.impl = args.schedule
+    if args.share_decode and ctx.world > 1:
+        sess.share_decode(ctx)
     per_step = ctx.world if afr else 1  # 1024^2 frames completed per step, whole job
 
     def cam(f):
@@ -638,7 +643,9 @@ def main():
             "march": args.march if args.schedule is None else f"impl {args.schedule}",
             "parallelism": (f"alternate-frame rendering x{ctx.world} (private cache per GPU, NCCL frame gather)" if afr
                             else f"sort-first film-row bands x{ctx.world} (private cache per GPU, RGBA8 bands "
-                                 f"gathered to rank 0 over NCCL on a comm stream)" if ctx.world > 1 else "single GPU"),
+                                 f"gathered to rank 0 over NCCL on a comm stream"
+                                 f"{'; brick decodes shared across ranks' if args.share_decode else ''})"
+                            if ctx.world > 1 else "single GPU"),
             "roofline": roofline(samples_all, march_all, launches_all, peak, peak_src, args.march,
                                  (march_all / ctx.world) / total_ms if total_ms else None),
             "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "macro_grid": macro_info,
