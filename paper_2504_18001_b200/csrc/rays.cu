@@ -50,6 +50,11 @@ struct RmCfg {
     double4* ray_a;                      // [n] dx, dy, dz, t_enter of the box-hitting rays
     double2* ray_b;                      // [n] t_exit, (local pixel, film pixel) as two int32
     int* n_rays;                         // rays in the list (written by k_ray_setup)
+    // a mapped host image: k_ray_setup lists the background pixels from the end of ray_b
+    // and k_bg_fill stores them on a side stream while the march runs
+    int* n_bg;
+    int bg_list;
+    long long cap;
 };
 
 // workspace after frame_ws_layout(0, ...): the ray list
@@ -121,9 +126,20 @@ __global__ void __launch_bounds__(256) k_ray_setup(const __grid_constant__ VcbFr
             film_coord(x, film_row, W, H, fx, fy);
             r = make_ray(fx, fy, p.cam);
             keep = r.keep;
-            if (!keep) reinterpret_cast<float4*>(p.image)[frame_pixel(p, (long long)yl * W + x)] = bgv;
+            if (!keep && !cfg.bg_list) reinterpret_cast<float4*>(p.image)[frame_pixel(p, (long long)yl * W + x)] = bgv;
         }
         const unsigned kb = __ballot_sync(0xffffffffu, keep);
+        if (cfg.bg_list) {
+            const bool bgp = x < W && yl < rows && !keep;
+            const unsigned bm = __ballot_sync(0xffffffffu, bgp);
+            int bb = 0;
+            if (lane == 0 && bm) bb = atomicAdd(cfg.n_bg, __popc(bm));
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            if (bgp) {
+                const long long j = cfg.cap - 1 - (bb + __popc(bm & ((1u << lane) - 1u)));
+                cfg.ray_b[j] = make_double2(0.0, __hiloint2double(0, yl * W + x));
+            }
+        }
         int base = 0;
         if (lane == 0 && kb) base = atomicAdd(cfg.n_rays, __popc(kb));
         base = __shfl_sync(0xffffffffu, base, 0);
@@ -132,6 +148,18 @@ __global__ void __launch_bounds__(256) k_ray_setup(const __grid_constant__ VcbFr
             cfg.ray_a[j] = make_double4(r.dx, r.dy, r.dz, r.t0);
             cfg.ray_b[j] = make_double2(r.t1, __hiloint2double(film_row * W + x, yl * W + x));
         }
+    }
+}
+
+// The background pixels k_ray_setup listed (bg_list), stored into the mapped host image
+// by one CTA on a side stream while the march runs on the other SMs: their PCIe writes
+// (~40% of a 1024^2 frame) then overlap the march instead of preceding it.
+__global__ void __launch_bounds__(1024) k_bg_fill(const __grid_constant__ VcbFrameParams p, RmCfg cfg) {
+    const float4 bgv = make_float4((float)p.bg[0], (float)p.bg[1], (float)p.bg[2], 0.0f);
+    const long long n = __ldcg(cfg.n_bg);
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const double2 rb = __ldcs(cfg.ray_b + (cfg.cap - 1 - i));
+        reinterpret_cast<float4*>(p.image)[frame_pixel(p, __double2loint(rb.y))] = bgv;
     }
 }
 
@@ -458,6 +486,24 @@ static const void* ray_kernel(int mode, int nt, int fast) {
                      : mode == 2 ? (const void*)k_ray_march<2, 512, 0> : (const void*)k_ray_march<0, 512, 0>;
 }
 
+// The side stream (and its two events) k_bg_fill runs on, one set per device.
+static bool bg_side_stream(cudaStream_t* s, cudaEvent_t* a, cudaEvent_t* b) {
+    static cudaStream_t streams[64] = {};
+    static cudaEvent_t evs[64][2] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    if (streams[dev] == nullptr) {
+        if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&evs[dev][0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&evs[dev][1], cudaEventDisableTiming) != cudaSuccess)
+            return false;
+    }
+    *s = streams[dev];
+    *a = evs[dev][0];
+    *b = evs[dev][1];
+    return true;
+}
+
 // nt: threads per CTA (one CTA per SM); max_skip: see advance_impl
 int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launches, cudaEvent_t* ev, int* ev_used,
                      int nt, int max_skip) {
@@ -476,6 +522,13 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     cfg.tiles_x = (p.cam.width + 7) / 8;
     cfg.n_tickets = (long long)cfg.tiles_x * ((p.cam.rows + 3) / 4) * 32;
     cfg.n_rays = &w.ctr->pad[0];
+    cfg.n_bg = &w.ctr->pad[4];
+    cfg.cap = npix;
+    {
+        cudaPointerAttributes pa;
+        cfg.bg_list = cudaPointerGetAttributes(&pa, p.image) == cudaSuccess && pa.type == cudaMemoryTypeHost ? 1 : 0;
+        cudaGetLastError();
+    }
     if (cfg.n_tickets >= (1ll << 31)) return set_error("march_frame: %lld pixels exceed the ticket range", (long long)npix);
     if (((uintptr_t)p.lut | (uintptr_t)p.mu) & 15)
         return set_error("march_frame: the LUT and majorant arrays must be 16-byte aligned (TMA)");
@@ -527,16 +580,28 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
         k_coarse_occ<<<grid_for((int64_t)cfg.coarse_words * 32, 256), 256, 0, st>>>(
             p.mu, (int)p.adv.gx, (int)p.adv.gy, (int)p.adv.gz, cfg.coarse, cfg.coarse_words);
     k_ray_setup<<<grid_for(cfg.n_tickets, 256), 256, 0, st>>>(p, cfg);
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_setup = nullptr, ev_bg = nullptr;
+    if (cfg.bg_list && bg_side_stream(&side, &ev_setup, &ev_bg)) {
+        cudaEventRecord(ev_setup, st);
+        cudaStreamWaitEvent(side, ev_setup, 0);
+        k_bg_fill<<<1, 1024, 0, side>>>(p, cfg);
+        cudaEventRecord(ev_bg, side);
+    } else if (cfg.bg_list) {
+        return set_error("march_frame: no side stream for the background pixels");
+    }
     VcbFrameParams pc = p;
     FrameCounters* ctr = w.ctr;
     void* args[3] = {&pc, &ctr, &cfg};
-    cudaError_t e = cudaLaunchKernel(fn, G, nt, args, off, st);
+    // with a mapped image one SM is left to k_bg_fill
+    cudaError_t e = cudaLaunchKernel(fn, cfg.bg_list ? G - 1 : G, nt, args, off, st);
+    if (cfg.bg_list) cudaStreamWaitEvent(st, ev_bg, 0);
     if (ev) {
         cudaEventRecord(ev[1], st);
         *ev_used = 1;
     }
     if (e != cudaSuccess) return set_error("march_frame: ray kernel launch: %s", cudaGetErrorString(e));
-    *launches = fast == 2 ? 3 : 2;
+    *launches = (fast == 2 ? 3 : 2) + (cfg.bg_list ? 1 : 0);
     return check_launch("march_frame(rays)");
 }
 
