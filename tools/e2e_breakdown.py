@@ -29,10 +29,13 @@ def main(preroll=60, n=50):
         s.render_frame()
     s.timing = True
     med = statistics.median
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if "--flush" in sys.argv else None
     for mode in ("device", "host", "device", "host"):
         wall, mar = [], []
         for f in range(preroll, preroll + n):
             c = traj.camera_at(f)
+            if flush is not None:
+                flush.zero_()
             torch.cuda.synchronize()
             h0 = time.perf_counter()
             s.set_camera(c)
@@ -44,7 +47,7 @@ def main(preroll=60, n=50):
                 s.collect_record(h0)
             wall.append((time.perf_counter() - h0) * 1e6)
             mar.append(s._ev_t0.elapsed_time(s._ev_t1) * 1e3)
-        print(f"{mode:6s}: wall {med(wall):.1f} us, frame kernels {med(mar):.1f} us, rest {med(wall) - med(mar):.1f} us")
+        print(f"{'flush ' if flush is not None else ''}{mode:6s}: wall {med(wall):.1f} us, frame kernels {med(mar):.1f} us, rest {med(wall) - med(mar):.1f} us")
 
 
 if __name__ == "__main__":
