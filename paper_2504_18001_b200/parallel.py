@@ -246,7 +246,7 @@ class BrickShare:
     per key).  NCCL all-gathers on the session stream; gloo (ranks sharing a GPU in the
     functional checks) goes through host memory."""
 
-    def __init__(self, ctx: Ctx, sess):
+    def __init__(self, ctx: Ctx, sess, cap=None):
         c = sess.cache
         if c is None:
             raise ValueError("brick sharing needs a cached session")
@@ -255,7 +255,7 @@ class BrickShare:
         mr = int(c.sched.max_requests)
         b3 = int(c.geom.b) ** 3
         W = ctx.world
-        self.mr, self.cap, self.b3 = mr, mr, b3
+        self.mr, self.cap, self.b3 = mr, int(cap) if cap is not None else mr, b3  # cap: slab bricks per owner
         e = lambda n, dt: torch.empty(n, dtype=dt, device=dev)
         self.keys = e(mr + 1, torch.int64)
         self.keys_all = e(W * (mr + 1), torch.int64)

@@ -154,7 +154,7 @@ class RenderSession:
             raise ValueError(f"unknown march schedule {name!r} (parity | throughput)")
         self.impl = self.MARCH_SCHEDULES[name]
 
-    def share_decode(self, ctx):
+    def share_decode(self, ctx, cap=None):
         """Decode each frame's brick batch jointly with the other ranks of `ctx`
         (parallel.BrickShare): every distinct requested brick is decoded once, by its
         owner rank, and all-gathered.  Same cache state as decoding alone; with
@@ -162,7 +162,7 @@ class RenderSession:
         from .parallel import BrickShare
 
         self._sync_decode()
-        self._share = BrickShare(ctx, self) if ctx is not None else None
+        self._share = BrickShare(ctx, self, cap) if ctx is not None else None
 
     def set_band(self, row0: int, row_step: int):
         """Render only film rows row0 + j*row_step (one rank's share of a frame)."""

@@ -27,14 +27,15 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
-@pytest.mark.parametrize("name", ["pressure", "inr64"])
-def test_shared_decode_world1_matches_reference(name):
+@pytest.mark.parametrize("name,cap", [("pressure", None), ("inr64", None), ("pressure", 3)])
+def test_shared_decode_world1_matches_reference(name, cap):
+    """cap=3: most of each batch overflows the owner's slab and is decoded locally."""
     from gpu_runner import run_gpu_session
     from paper_2504_18001_b200 import parallel
 
     g = load_golden(f"session_{name}.npz")
     exact = name == "pressure"
-    share = lambda sess: sess.share_decode(parallel.Ctx())
+    share = lambda sess: sess.share_decode(parallel.Ctx(), cap=cap)
     for f, img, rec, sess in run_gpu_session(name, macro=(g["macro_vmin"], g["macro_vmax"]), setup=share):
         assert sess._share is not None
         st = sess.debug_state()
@@ -71,3 +72,61 @@ def test_shared_decode_across_ranks_equals_alone(tmp_path, world, name):
         owned += int(d["owned_total"])
     # the ranks' batches overlap: together they decoded fewer bricks than alone
     assert 0 < owned < alone_total
+
+
+def _splitmix64(x):
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+@pytest.mark.parametrize("world,mr,cap,seed", [(3, 12, 12, 0), (3, 12, 2, 1), (4, 40, 5, 2), (1, 7, 3, 3)])
+def test_share_plan_matches_restatement(world, mr, cap, seed):
+    """vcb_share_plan against a direct restatement: owner = splitmix64(key) % world,
+    slot = rank among the owner's distinct keys, keys past `cap` decoded locally
+    (small caps force the overflow path); duplicates across ranks decoded once."""
+    import torch
+
+    from paper_2504_18001_b200 import _native as N
+
+    rng = np.random.default_rng(seed)
+    pool = rng.choice(10_000, size=mr * world, replace=False)
+    rows = np.full((world, mr + 1), -1, dtype=np.int64)
+    for q in range(world):
+        n = int(rng.integers(0, mr + 1))
+        keys = rng.choice(pool[: max(1, mr * world // 2)], size=min(n, mr * world // 2), replace=False)[:mr]
+        rows[q, 0] = len(keys)
+        rows[q, 1:1 + len(keys)] = keys
+    dev = torch.device("cuda")
+    all_keys = torch.from_numpy(rows.ravel()).to(dev)
+    for rank in range(world):
+        own = torch.full((cap,), -1, dtype=torch.int64, device=dev)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        src = torch.empty(mr, dtype=torch.int32, device=dev)
+        ovf_keys = torch.full((mr,), -1, dtype=torch.int64, device=dev)
+        ovf_idx = torch.full((mr,), -1, dtype=torch.int32, device=dev)
+        N.call("vcb_share_plan", all_keys.data_ptr(), world, rank, mr, cap, own.data_ptr(), counts.data_ptr(),
+               src.data_ptr(), ovf_keys.data_ptr(), ovf_idx.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        distinct = sorted({int(k) for q in range(world) for k in rows[q, 1:1 + rows[q, 0]]})
+        owner = {k: _splitmix64(k) % world for k in distinct}
+        slots = {k: sorted(v for v in distinct if owner[v] == owner[k]).index(k) for k in distinct}
+        mine = [k for k in distinct if owner[k] == rank]
+        want_own = [k for k in mine if slots[k] < cap]
+        assert int(counts[0]) == len(want_own)
+        np.testing.assert_array_equal(own.cpu().numpy()[: len(want_own)], want_own)
+        n_mine = int(rows[rank, 0])
+        got_src = src.cpu().numpy()
+        ovf = {}
+        for i in range(n_mine):
+            k = int(rows[rank, 1 + i])
+            if slots[k] < cap:
+                assert got_src[i] == owner[k] * cap + slots[k]
+            else:
+                assert got_src[i] == -1
+                ovf[i] = k
+        assert int(counts[1]) == len(ovf)
+        oi, ok = ovf_idx.cpu().numpy()[: len(ovf)], ovf_keys.cpu().numpy()[: len(ovf)]
+        assert {int(i): int(k) for i, k in zip(oi, ok)} == ovf
