@@ -282,6 +282,8 @@ int32_t vcb_shade_pass(int64_t n, const int64_t *rows, const float *values, cons
 
 /* diagnostics: the shade's accurate pow, out[i] = x[i]**y[i] (x in (0,1], y > 0) */
 int32_t vcb_debug_pow(int64_t n, const double *x, const double *y, double *out, void *stream);
+/* The same pow through its double-double phase only (the fast phase's cross-check). */
+int32_t vcb_debug_pow_accurate(int64_t n, const double *x, const double *y, double *out, void *stream);
 
 /* ---- field / decoder ABI */
 int32_t vcb_field_points(const VcbField *f, int64_t n, const double *pos, float *out, int32_t *nonfinite,

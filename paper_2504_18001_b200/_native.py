@@ -123,6 +123,7 @@ _PROTOS = {
     "vcb_probe_pass": (i32, [i64, vp, vp, vp, C.POINTER(VcbProbeStatic), vp, vp, vp, i64, vp, vp, vp, vp, vp]),
     "vcb_shade_pass": (i32, [i64, vp, vp, vp, vp, i64, i32, f64, f64, vp, vp, vp, vp]),
     "vcb_debug_pow": (i32, [i64, vp, vp, vp, vp]),
+    "vcb_debug_pow_accurate": (i32, [i64, vp, vp, vp, vp]),
     "vcb_field_points": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),
     "vcb_field_bricks": (i32, [C.POINTER(VcbField), C.POINTER(VcbBrickGeom), i64, vp, vp, vp, vp]),
     "vcb_inr_points_tc": (i32, [C.POINTER(VcbField), i64, vp, vp, vp, vp]),

@@ -114,9 +114,9 @@ __global__ void k_shade_pass(int64_t n, const int64_t* __restrict__ rows, const 
     }
 }
 
-__global__ void k_pow_dd(int64_t n, const double* x, const double* y, double* out) {
+__global__ void k_pow_dd(int64_t n, const double* x, const double* y, double* out, int accurate) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = pow_dd(x[i], y[i]);
+        out[i] = accurate ? pow_dd_accurate(x[i], y[i]) : pow_dd(x[i], y[i]);
 }
 
 // ----------------------------------------------------------------- frame march
@@ -408,8 +408,14 @@ extern "C" int32_t vcb_raygen_pass(int64_t n, const double* base, const double* 
 
 extern "C" int32_t vcb_debug_pow(int64_t n, const double* x, const double* y, double* out, void* stream) {
     if (n <= 0) return 0;
-    k_pow_dd<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, y, out);
+    k_pow_dd<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, y, out, 0);
     return check_launch("debug_pow");
+}
+
+extern "C" int32_t vcb_debug_pow_accurate(int64_t n, const double* x, const double* y, double* out, void* stream) {
+    if (n <= 0) return 0;
+    k_pow_dd<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, y, out, 1);
+    return check_launch("debug_pow_accurate");
 }
 
 extern "C" int32_t vcb_advance_pass(int64_t n, const double* o, const double* d, const double* t_en,
