@@ -31,6 +31,7 @@
 // whole warp runs the tensor-core inference (mlp_warp.cuh, 32 samples per call)
 // whenever any lane holds a miss, so its values are the parity path's.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fields.cuh"
@@ -55,6 +56,7 @@ struct RmCfg {
     int* n_bg;
     int bg_list;
     long long cap;
+    int spec_fb;                         // speculative coarser-level loads after a fallback
 };
 
 // workspace after frame_ws_layout(0, ...): the ray list
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t* occ = nullptr;
     const uint32_t lut_bytes = s_lut ? (uint32_t)p.lut_size * 16u : 0u;
     const uint32_t mu_bytes = 0u;  // (the majorant grid: by the threads, measured faster at config 2)
-    const uint32_t co_bytes = kFast == 2 ? ((uint32_t)cfg.coarse_words * 4u + 15u) & ~15u : 0u;
+    const uint32_t co_bytes = kFast >= 2 ? ((uint32_t)cfg.coarse_words * 4u + 15u) & ~15u : 0u;
     if (threadIdx.x == 0) {
         tma_stage_begin(&tma_bar, lut_bytes + mu_bytes + co_bytes);
         if (lut_bytes) tma_stage_copy(s_lut, p.lut, lut_bytes, &tma_bar);
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         occ = o;
     }
+    if (kFast == 3) occ = reinterpret_cast<const uint32_t*>(dsm + cfg.sm_occ);
     MlpSmem mlp;
     mlp.w = mlp.b = nullptr;
     const MlpFrag* mfrag = nullptr;
@@ -264,6 +267,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     // per-lane ray state
     bool has = false;
+    bool fbprev = false;     // the ray's last sample was not served at its requested LoD
     int k = 0;               // samples taken by the lane's ray (the wavefront iteration index)
     long long pix = 0;       // local (band) pixel index
     double dx = 0.0, dy = 0.0, dz = 0.0, ten = 0.0, tex = 0.0;
@@ -359,20 +363,26 @@ __global__ void __launch_bounds__(NT, 1)
                     const double ex = DSUB(a.px, ox), ey = DSUB(a.py, oy), ez = DSUB(a.pz, oz);
                     dist = __dsqrt_rn(DADD(DADD(DMUL(ex, ex), DMUL(ey, ey)), DMUL(ez, ez)));
                 }
-                int rq, slot;
-                const int sv = probe_one(a.px, a.py, a.pz, dist, u, p.probe, p.table, p.pool,
-                                         (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv);
+                int rq, slot, rflat;
+                const int sv = probe_one<kFast ? 1 : -1>(a.px, a.py, a.pz, dist, u, p.probe, p.table, p.pool,
+                                         (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv, &rflat,
+                                         kFast && cfg.spec_fb && fbprev);
+                fbprev = sv != rq;
                 if (sv != rq) {
-                    // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
-                    const i64 span = p.probe.b << rq;
-                    const double nx = clampd(DSUB(DMUL(a.px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
-                    const double ny = clampd(DSUB(DMUL(a.py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
-                    const double nz = clampd(DSUB(DMUL(a.pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
-                    const int4 q = sm.lv[rq];
-                    const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, q.x - 1);
-                    const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, q.y - 1);
-                    const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, q.z - 1);
-                    warp_aggregated_add(p.miss_count, (i64)q.w + bx + (i64)q.x * (by + (i64)q.y * bz));
+                    if (kFast || p.probe.b_pow2 != 0) {
+                        warp_aggregated_add(p.miss_count, (i64)rflat);  // the probe's requested brick
+                    } else {
+                        // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
+                        const i64 span = p.probe.b << rq;
+                        const double nx = clampd(DSUB(DMUL(a.px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
+                        const double ny = clampd(DSUB(DMUL(a.py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
+                        const double nz = clampd(DSUB(DMUL(a.pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
+                        const int4 q = sm.lv[rq];
+                        const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, q.x - 1);
+                        const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, q.y - 1);
+                        const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, q.z - 1);
+                        warp_aggregated_add(p.miss_count, (i64)q.w + bx + (i64)q.x * (by + (i64)q.y * bz));
+                    }
                 }
                 if (sv < 0) {
                     needinf = 1;
@@ -472,6 +482,9 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 static const void* ray_kernel(int mode, int nt, int fast) {
+    if (fast == 3)
+        return mode == 1 ? (const void*)k_ray_march<1, 512, 3>
+                         : mode == 2 ? (const void*)k_ray_march<2, 512, 3> : (const void*)k_ray_march<0, 512, 3>;
     if (fast == 2)
         return mode == 1 ? (const void*)k_ray_march<1, 512, 2>
                          : mode == 2 ? (const void*)k_ray_march<2, 512, 2> : (const void*)k_ray_march<0, 512, 2>;
@@ -551,12 +564,19 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     }
     const long long cells = p.adv.gx * p.adv.gy * p.adv.gz;
     cfg.sm_mu = cfg.sm_occ = -1;
-    if (off + 16 + cells * 4 <= kSmemMax) cfg.sm_mu = take((int)cells * 4);
+    // CINR_FORCE_SUPERCELL (tests only): the large-grid specialisation (super-cell bits,
+    // super-cell jumps) on any macro grid, so small scenes exercise it against the oracle
+    const bool force_sc = getenv("CINR_FORCE_SUPERCELL") != nullptr;
+    if (force_sc) {
+    } else if (off + 16 + cells * 4 <= kSmemMax) cfg.sm_mu = take((int)cells * 4);
     else if (p.adv.skip_empty && off + 16 + ((cells + 31) >> 5) * 4 <= kSmemMax)
         cfg.sm_occ = take((int)(((cells + 31) >> 5) * 4));
-    int fast = (cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty) ? 1 : 0;
+    // (the specialised kernels also assume power-of-two brick spans: shift-based LoD walk)
+    const bool spec_ok = p.adv.adaptive && p.adv.skip_empty && p.probe.b_pow2 != 0;
+    int fast = (cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && spec_ok) ? 1 : 0;
     cfg.coarse_words = 0;
-    if (!fast && cfg.sm_occ < 0 && cfg.sm_lut >= 0 && p.adv.adaptive && p.adv.skip_empty && cells > 0) {
+    cfg.spec_fb = getenv("CINR_SPEC_FB") != nullptr ? 1 : 0;
+    if (!fast && cfg.sm_occ < 0 && cfg.sm_lut >= 0 && spec_ok && cells > 0) {
         // majorants too large for shared memory (4096^3: 256^3 cells): super-cell bits
         const long long nsc = (long long)((p.adv.gx + 3) / 4) * ((p.adv.gy + 3) / 4) * ((p.adv.gz + 3) / 4);
         const int words = (int)((nsc + 31) / 32);
@@ -567,8 +587,18 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
             fast = 2;
         }
     }
+    if (fast == 1 && getenv("CINR_KFAST3") != nullptr) {
+        // majorants in shared memory plus super-cell bits: jumps over empty super-cells
+        const long long nsc = (long long)((p.adv.gx + 3) / 4) * ((p.adv.gy + 3) / 4) * ((p.adv.gz + 3) / 4);
+        const int words = (int)((nsc + 31) / 32);
+        if (off + 16 + ((words * 4 + 15) & ~15) <= kSmemMax) {
+            cfg.sm_occ = take((words * 4 + 15) & ~15);
+            cfg.coarse_words = words;
+            fast = 3;
+        }
+    }
     if (mode == 2 || !fast) nt = 512;
-    if (fast == 2) nt = 512;
+    if (fast >= 2) nt = 512;
     if (off > kSmemMax) return set_error("march_frame: %d B of shared memory needed", off);
     const void* fn = ray_kernel(mode, nt, fast);
     const int per_sm = kernel_ctas_per_sm(fn, nt, off);
@@ -576,7 +606,7 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     cudaMemsetAsync(w.ctr, 0, sizeof(FrameCounters), st);
     const int G = device_sms();
     if (ev) cudaEventRecord(ev[0], st);
-    if (fast == 2)
+    if (fast >= 2)
         k_coarse_occ<<<grid_for((int64_t)cfg.coarse_words * 32, 256), 256, 0, st>>>(
             p.mu, (int)p.adv.gx, (int)p.adv.gy, (int)p.adv.gz, cfg.coarse, cfg.coarse_words);
     k_ray_setup<<<grid_for(cfg.n_tickets, 256), 256, 0, st>>>(p, cfg);
@@ -601,7 +631,7 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
         *ev_used = 1;
     }
     if (e != cudaSuccess) return set_error("march_frame: ray kernel launch: %s", cudaGetErrorString(e));
-    *launches = (fast == 2 ? 3 : 2) + (cfg.bg_list ? 1 : 0);
+    *launches = (fast >= 2 ? 3 : 2) + (cfg.bg_list ? 1 : 0);
     return check_launch("march_frame(rays)");
 }
 

@@ -666,20 +666,24 @@ __global__ void __launch_bounds__(NT, 1)
                             const double ex = DSUB(px, c.ox), ey = DSUB(py, c.oy), ez = DSUB(pz, c.oz);
                             dist = __dsqrt_rn(DADD(DADD(DMUL(ex, ex), DMUL(ey, ey)), DMUL(ez, ez)));
                         }
-                        int rq, slot;
+                        int rq, slot, rflat;
                         const int sv = probe_one(px, py, pz, dist, u, p.probe, p.table, p.pool,
-                                                 (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv);
+                                                 (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv, &rflat);
                         if (sv != rq) {
-                            // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
-                            const i64 span = p.probe.b << rq;
-                            const double nx = clampd(DSUB(DMUL(px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
-                            const double ny = clampd(DSUB(DMUL(py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
-                            const double nz = clampd(DSUB(DMUL(pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
-                            const int4 q = sm.lv[rq];
-                            const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, q.x - 1);
-                            const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, q.y - 1);
-                            const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, q.z - 1);
-                            warp_aggregated_add(p.miss_count, (i64)q.w + bx + (i64)q.x * (by + (i64)q.y * bz));
+                            if (p.probe.b_pow2 != 0) {
+                                warp_aggregated_add(p.miss_count, (i64)rflat);  // the probe's requested brick
+                            } else {
+                                // mrpd.py:215-225 miss filing at the requested LoD (native clipped, P6)
+                                const i64 span = p.probe.b << rq;
+                                const double nx = clampd(DSUB(DMUL(px, p.probe.vx), 0.5), 0.0, DSUB(p.probe.vx, 1.0));
+                                const double ny = clampd(DSUB(DMUL(py, p.probe.vy), 0.5), 0.0, DSUB(p.probe.vy, 1.0));
+                                const double nz = clampd(DSUB(DMUL(pz, p.probe.vz), 0.5), 0.0, DSUB(p.probe.vz, 1.0));
+                                const int4 q = sm.lv[rq];
+                                const i64 bx = clampi((i64)floor(cell_div(DADD(nx, 1.0), (double)span)), 0, q.x - 1);
+                                const i64 by = clampi((i64)floor(cell_div(DADD(ny, 1.0), (double)span)), 0, q.y - 1);
+                                const i64 bz = clampi((i64)floor(cell_div(DADD(nz, 1.0), (double)span)), 0, q.z - 1);
+                                warp_aggregated_add(p.miss_count, (i64)q.w + bx + (i64)q.x * (by + (i64)q.y * bz));
+                            }
                         }
                         if (sv < 0) {
                             queued = 1;

@@ -135,6 +135,72 @@ def test_config2_1024_resumed_frame_vs_oracle(march):
     assert rec.samples > 10_000_000
 
 
+def test_config3_coherent_empty_space_supercell_jumps_vs_oracle():
+    """4096^3 with spatially coherent empty space (blocks of 8^3 macro cells, 40% empty,
+    plus everything outside a ball): the throughput kernel leaves whole empty 4x4x4
+    super-cells in one step there (advance_impl<2>); the resumed frame must still equal
+    the oracle's cell-by-cell walk bit for bit."""
+    from gpu_runner import macro_from
+
+    dims = (4096,) * 3
+    rng = np.random.default_rng(11)
+    blocks = rng.random((32, 32, 32)) < 0.4
+    empty = np.repeat(np.repeat(np.repeat(blocks, 8, 0), 8, 1), 8, 2)
+    i = (np.arange(256) + 0.5 - 128.0) ** 2
+    empty |= (i[:, None, None] + i[None, :, None] + i[None, None, :]) > 118.0 ** 2
+    vmax = np.where(empty, 0.2, 1.0).astype(np.float32)
+    vmin = np.zeros_like(vmax)
+    rec = _resumed_frame_check(dims, 512, 24, "throughput", 12, (vmin, vmax), macro_from(dims, vmin, vmax))
+    assert rec.samples > 1_000_000
+
+
+def test_config2_forced_supercell_kernel_equals_default():
+    """The benched config 2 (512^3 INR, its own macro grid: coherent empty space) with the
+    large-grid specialisation forced (CINR_FORCE_SUPERCELL: super-cell bits + jumps over
+    empty super-cells) renders the same frames and cache state as the default
+    shared-memory-majorant kernel, over a cold-cache orbit."""
+    import os
+
+    from gpu_runner import product_inr
+    from paper_2504_18001_b200 import macrocell
+    from paper_2504_18001_b200.harness import OrbitTrajectory
+    from paper_2504_18001_b200.session import RenderSession, SessionConfig
+
+    import paper_2504_18001_b200 as P
+
+    dims = (512,) * 3
+    fld = product_inr(dims).as_field()
+    mg = macrocell.build(fld, dims, 16)
+    traj = OrbitTrajectory((0.5, 0.5, 0.5), 2.2, 120, width=512, height=512)
+
+    def run(force):
+        if force:
+            os.environ["CINR_FORCE_SUPERCELL"] = "1"
+        try:
+            cfg = SessionConfig(cached=True, loader="inline", cache=P.CacheConfig(brick_size=16, pool_dims=(32,) * 3),
+                                scheduler=P.SchedulerConfig(max_requests=40), policy=P.LodPolicy(1.2, 20),
+                                settings=P.RenderSettings(), seed=0)
+            s = RenderSession(fld, P.warm_body(0.5, 0.9), traj.camera_at(0), cfg, macro=mg, march="throughput")
+            out = []
+            for f in range(0, 48, 4):
+                s.set_camera(traj.camera_at(f))
+                img, rec = s.render_frame()
+                st = s.cache.dump()
+                out.append((img.copy(), (rec.samples, rec.true_misses, rec.fallback_hits, rec.exact_hits,
+                                         rec.bricks_loaded), {k: st[k].copy() for k in ("tables", "owner", "last_used",
+                                                                                        "entries")}))
+            return out
+        finally:
+            os.environ.pop("CINR_FORCE_SUPERCELL", None)
+
+    a, b = run(False), run(True)
+    for f, ((ia, ra, sa), (ib, rb, sb)) in enumerate(zip(a, b)):
+        assert ra == rb, f"frame {f}: {ra} vs {rb}"
+        np.testing.assert_array_equal(ia, ib, err_msg=f"frame {f} image")
+        for k in sa:
+            np.testing.assert_array_equal(sa[k], sb[k], err_msg=f"frame {f} {k}")
+
+
 @pytest.mark.parametrize("march,res", [("parity", 1024), ("throughput", 512)])
 def test_config3_4096_resumed_frame_vs_oracle(march, res):
     """4096^3 virtual volume (19.4 M bricks, paged MRPD distances on the reference

@@ -74,6 +74,14 @@ def test_mode_off_throughput_equals_parity(base):
         scene_specs.SESSION_SPECS.pop(name, None)
 
 
+@pytest.mark.parametrize("base", ["pressure", "lattice64", "events"])
+def test_mode_off_supercell_kernel_equals_parity(base, monkeypatch):
+    """The large-grid specialisation (super-cell bits, jumps over empty super-cells)
+    forced on the small golden scenes: still the parity schedule's state bit for bit."""
+    monkeypatch.setenv("CINR_FORCE_SUPERCELL", "1")
+    test_mode_off_throughput_equals_parity(base)
+
+
 @pytest.mark.parametrize("base", ["pressure", "lattice64", "lattice64_paged", "events", "lattice64_fifo", "inr64"])
 def test_pixel_lane_sessions_vs_oracle(base):
     """Stochastic LoD with pixel lanes: CUDA throughput schedule == oracle(rng="pixel")."""
