@@ -56,7 +56,6 @@ struct RmCfg {
     int* n_bg;
     int bg_list;
     long long cap;
-    int spec_fb;                         // speculative coarser-level loads after a fallback
 };
 
 // workspace after frame_ws_layout(0, ...): the ray list
@@ -242,7 +241,6 @@ __global__ void __launch_bounds__(NT, 1)
         }
         occ = o;
     }
-    if (kFast == 3) occ = reinterpret_cast<const uint32_t*>(dsm + cfg.sm_occ);
     MlpSmem mlp;
     mlp.w = mlp.b = nullptr;
     const MlpFrag* mfrag = nullptr;
@@ -267,7 +265,6 @@ __global__ void __launch_bounds__(NT, 1)
 
     // per-lane ray state
     bool has = false;
-    bool fbprev = false;     // the ray's last sample was not served at its requested LoD
     int k = 0;               // samples taken by the lane's ray (the wavefront iteration index)
     long long pix = 0;       // local (band) pixel index
     double dx = 0.0, dy = 0.0, dz = 0.0, ten = 0.0, tex = 0.0;
@@ -365,9 +362,7 @@ __global__ void __launch_bounds__(NT, 1)
                 }
                 int rq, slot, rflat;
                 const int sv = probe_one<kFast ? 1 : -1>(a.px, a.py, a.pz, dist, u, p.probe, p.table, p.pool,
-                                         (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv, &rflat,
-                                         kFast && cfg.spec_fb && fbprev);
-                fbprev = sv != rq;
+                                         (long long*)p.last_used, p.cache_frame, v, rq, slot, sm.lv, &rflat);
                 if (sv != rq) {
                     if (kFast || p.probe.b_pow2 != 0) {
                         warp_aggregated_add(p.miss_count, (i64)rflat);  // the probe's requested brick
@@ -482,9 +477,6 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 static const void* ray_kernel(int mode, int nt, int fast) {
-    if (fast == 3)
-        return mode == 1 ? (const void*)k_ray_march<1, 512, 3>
-                         : mode == 2 ? (const void*)k_ray_march<2, 512, 3> : (const void*)k_ray_march<0, 512, 3>;
     if (fast == 2)
         return mode == 1 ? (const void*)k_ray_march<1, 512, 2>
                          : mode == 2 ? (const void*)k_ray_march<2, 512, 2> : (const void*)k_ray_march<0, 512, 2>;
@@ -575,7 +567,6 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
     const bool spec_ok = p.adv.adaptive && p.adv.skip_empty && p.probe.b_pow2 != 0;
     int fast = (cfg.sm_mu >= 0 && cfg.sm_lut >= 0 && spec_ok) ? 1 : 0;
     cfg.coarse_words = 0;
-    cfg.spec_fb = getenv("CINR_SPEC_FB") != nullptr ? 1 : 0;
     if (!fast && cfg.sm_occ < 0 && cfg.sm_lut >= 0 && spec_ok && cells > 0) {
         // majorants too large for shared memory (4096^3: 256^3 cells): super-cell bits
         const long long nsc = (long long)((p.adv.gx + 3) / 4) * ((p.adv.gy + 3) / 4) * ((p.adv.gz + 3) / 4);
@@ -585,16 +576,6 @@ int launch_ray_frame(const VcbFrameParams& p, cudaStream_t st, long long* launch
             cfg.sm_occ = take((words * 4 + 15) & ~15);  // whole 16-byte rows for the TMA copy
             cfg.coarse_words = words;
             fast = 2;
-        }
-    }
-    if (fast == 1 && getenv("CINR_KFAST3") != nullptr) {
-        // majorants in shared memory plus super-cell bits: jumps over empty super-cells
-        const long long nsc = (long long)((p.adv.gx + 3) / 4) * ((p.adv.gy + 3) / 4) * ((p.adv.gz + 3) / 4);
-        const int words = (int)((nsc + 31) / 32);
-        if (off + 16 + ((words * 4 + 15) & ~15) <= kSmemMax) {
-            cfg.sm_occ = take((words * 4 + 15) & ~15);
-            cfg.coarse_words = words;
-            fast = 3;
         }
     }
     if (mode == 2 || !fast) nt = 512;
