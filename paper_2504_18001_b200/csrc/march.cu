@@ -498,8 +498,6 @@ extern "C" int32_t vcb_march_frame(const VcbFrameParams* pp, void* stream_) {
         if (p.impl == 12) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 640, 1);
         if (p.impl == 13) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 0);
         if (p.impl == 14) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 640, 2);
-        if (p.impl == 15) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 3);
-        if (p.impl == 16) return launch_ray_frame(p, st, &g_launches, ev, &g_ev_used, 512, 4);
         return launch_wave3_frame(p, st, &g_launches, ev, &g_ev_used, 384, 0);
     }
     const int64_t npix = (int64_t)p.cam.width * p.cam.rows;
